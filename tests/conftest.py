@@ -1,0 +1,41 @@
+"""Shared pytest wiring: markers, repo on sys.path, golden fixture loader."""
+
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+GOLDEN = ROOT / "tests" / "golden"
+REF_SRC = Path("/root/reference/pkg/src")
+sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a B200 (sm_100a) and the built CUDA library")
+    config.addinivalue_line("markers", "slow: long-running CPU test")
+
+
+def load_golden(name: str) -> dict:
+    with np.load(GOLDEN / f"{name}.npz") as z:
+        return {k: z[k] for k in z.files}
+
+
+def golden_cases() -> list[str]:
+    return sorted(p.stem for p in GOLDEN.glob("attn_*.npz"))
+
+
+def reference_available() -> bool:
+    return (REF_SRC / "lpattn" / "__init__.py").exists()
+
+
+@pytest.fixture(scope="session")
+def lpattn():
+    """The unmodified reference package, only where it exists (build container)."""
+    if not reference_available():
+        pytest.skip("reference source tree not present on this machine")
+    sys.path.insert(0, str(REF_SRC))
+    import lpattn as mod
+    return mod
