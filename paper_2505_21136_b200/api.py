@@ -1,0 +1,275 @@
+"""Host API: `sageattn` (north-star drop-in) and `attention_quantized` (reference mirror).
+
+Both run the sm_100a kernels through the C ABI (include/sa2pp.h).  PyTorch is
+only the device-memory and stream plumbing; all arithmetic of the path runs in
+the CUDA library.  There is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+import torch
+
+from . import _abi as A
+from .config import AttentionConfig, RangeConfig
+
+_DT = {torch.float32: A.SA2PP_F32, torch.float16: A.SA2PP_F16, torch.bfloat16: A.SA2PP_BF16}
+
+
+@dataclass
+class QuantizedTensors:
+    """Device tensors written by the prepass; layouts documented in include/sa2pp.h."""
+
+    q_codes: torch.Tensor      # int8  [B, Hq, Nq_pad, D]
+    q_scale: torch.Tensor      # f32   [B, Hq, nQT]
+    q_scale64: torch.Tensor    # f64   [B, Hq, nQT]
+    k_codes: torch.Tensor      # int8  [B, Hkv, Np, D]
+    v_codes: torch.Tensor      # uint8 [B, Hkv, D, Np] (E4M3, channel-major)
+    kv_meta: torch.Tensor      # f32   [B, Hkv, nKB, 4 + D]
+    kv_scale64: torch.Tensor   # f64   [B, Hkv, nKB, 1 + D]
+    bias: torch.Tensor         # f32   [B, Hq, Np]
+    bias_l2: torch.Tensor      # f32   [B, Hq, Np]
+    means: torch.Tensor        # f64   [B, Hq + Hkv, D]
+    workspace: torch.Tensor    # u8 scratch
+
+    @property
+    def k_scale64(self) -> torch.Tensor:
+        return self.kv_scale64[..., 0]
+
+    @property
+    def v_scale64(self) -> torch.Tensor:
+        return self.kv_scale64[..., 1:]
+
+    def struct(self) -> A.Quant:
+        return A.Quant(*(t.data_ptr() for t in (
+            self.q_codes, self.q_scale, self.q_scale64, self.k_codes, self.v_codes, self.kv_meta,
+            self.kv_scale64, self.bias, self.bias_l2, self.means)))
+
+
+def _problem(B, Hq, Hkv, N, D, *, causal, smoothing=True, qk_bits=8, pv_accum="fp16", depth=2,
+             expect_overflow=False, sm_scale=None, p_r=224.0, v_r=4.5) -> A.Problem:
+    return A.Problem(B, Hq, Hkv, N, D, int(bool(causal)), int(bool(smoothing)), qk_bits,
+                     A.SA2PP_ACC_F16 if pv_accum == "fp16" else A.SA2PP_ACC_F32, depth,
+                     int(bool(expect_overflow)), float(sm_scale) if sm_scale else 0.0,
+                     float(p_r), float(v_r))
+
+
+def alloc_quant(prob: A.Problem, device) -> QuantizedTensors:
+    sz = A.QuantSizes()
+    A.check(A.lib().sa2pp_quant_sizes(C_ref(prob), C_ref(sz)))
+    B, Hq, Hkv, N, D = prob.batch, prob.heads_q, prob.heads_kv, prob.seq_len, prob.head_dim
+    n_qt, n_kb = -(-N // 128), -(-N // 64)
+    nq_pad, np_ = n_qt * 128, n_kb * 64
+    e = lambda *shape, dt: torch.empty(shape, dtype=dt, device=device)  # noqa: E731
+    return QuantizedTensors(
+        q_codes=e(B, Hq, nq_pad, D, dt=torch.int8),
+        q_scale=e(B, Hq, n_qt, dt=torch.float32),
+        q_scale64=e(B, Hq, n_qt, dt=torch.float64),
+        k_codes=e(B, Hkv, np_, D, dt=torch.int8),
+        v_codes=e(B, Hkv, D, np_, dt=torch.uint8),
+        kv_meta=e(B, Hkv, n_kb, 4 + D, dt=torch.float32),
+        kv_scale64=e(B, Hkv, n_kb, 1 + D, dt=torch.float64),
+        bias=e(B, Hq, np_, dt=torch.float32),
+        bias_l2=e(B, Hq, np_, dt=torch.float32),
+        means=e(B, Hq + Hkv, D, dt=torch.float64),
+        workspace=e(max(int(sz.workspace), 16), dt=torch.uint8),
+    )
+
+
+def C_ref(x):
+    import ctypes
+    return ctypes.byref(x)
+
+
+def _bhnd_view(x: torch.Tensor, layout: str):
+    """(B, H, N, D, strides(b, h, n)) for an HND [B,H,N,D] or NHD [B,N,H,D] tensor."""
+    if x.dim() != 4:
+        raise ValueError(f"expected a 4-D tensor, got shape {tuple(x.shape)}")
+    if x.stride(-1) != 1:
+        raise ValueError("the head_dim axis must be contiguous")
+    if layout == "HND":
+        B, H, N, D = x.shape
+        return B, H, N, D, (x.stride(0), x.stride(1), x.stride(2))
+    if layout == "NHD":
+        B, N, H, D = x.shape
+        return B, H, N, D, (x.stride(0), x.stride(2), x.stride(1))
+    raise ValueError(f"tensor_layout must be 'HND' or 'NHD', got {layout!r}")
+
+
+def _stream_ptr(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def sageattn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, tensor_layout: str = "HND",
+             is_causal: bool = False, sm_scale: Optional[float] = None, *, pv_accum: str = "fp16",
+             smooth: bool = True, qk_bits: int = 8, p_r: float = 224.0, v_r: float = 4.5,
+             buffering_depth: int = 2, expect_overflow: bool = False,
+             out: Optional[torch.Tensor] = None, return_quant: bool = False,
+             report: Optional[torch.Tensor] = None, quant: Optional[QuantizedTensors] = None,
+             stream=None):
+    """SageAttention2++ forward on B200.
+
+    q: [B, Hq, N, D] (HND) or [B, N, Hq, D] (NHD); k, v: same with Hkv heads (Hq % Hkv == 0).
+    dtype float16 / bfloat16 / float32, CUDA.  Returns o with q's shape, layout and dtype.
+    Keyword-only extras: ``pv_accum="fp32"`` selects the SageAttention2 FP32-accumulator
+    baseline, ``return_quant=True`` also returns the prepass tensors for bit-exact checks.
+    """
+    if not (q.is_cuda and k.is_cuda and v.is_cuda):
+        raise ValueError("sageattn runs on CUDA tensors only (no CPU fallback)")
+    if not (q.dtype == k.dtype == v.dtype) or q.dtype not in _DT:
+        raise ValueError("q, k, v must share one dtype among float16, bfloat16, float32")
+    B, Hq, N, D, qs = _bhnd_view(q, tensor_layout)
+    Bk, Hkv, Nk, Dk, ks = _bhnd_view(k, tensor_layout)
+    Bv, Hv, Nv, Dv, vs = _bhnd_view(v, tensor_layout)
+    if (Bk, Nk, Dk) != (B, N, D) or (Bv, Hv, Nv, Dv) != (Bk, Hkv, Nk, Dk):
+        raise ValueError(f"Q/K/V shapes disagree: {tuple(q.shape)}, {tuple(k.shape)}, {tuple(v.shape)}")
+    prob = _problem(B, Hq, Hkv, N, D, causal=is_causal, smoothing=smooth, qk_bits=qk_bits,
+                    pv_accum=pv_accum, depth=buffering_depth, expect_overflow=expect_overflow,
+                    sm_scale=sm_scale, p_r=p_r, v_r=v_r)
+    A.check(A.lib().sa2pp_check_problem(C_ref(prob)))
+    qt = quant if quant is not None else alloc_quant(prob, q.device)
+    if out is None:
+        out = torch.empty_like(q)
+    B_, Ho, No, Do, os_ = _bhnd_view(out, tensor_layout)
+    if (B_, Ho, No, Do) != (B, Hq, N, D) or out.dtype not in _DT:
+        raise ValueError("out must match q's shape")
+    ins = A.Inputs(_DT[q.dtype], q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                   (A.C.c_int64 * 3)(*qs), (A.C.c_int64 * 3)(*ks), (A.C.c_int64 * 3)(*vs))
+    o = A.Output(_DT[out.dtype], out.data_ptr(), (A.C.c_int64 * 3)(*os_))
+    qs_struct = qt.struct()
+    rep_ptr = report.data_ptr() if report is not None else None
+    with torch.cuda.device(q.device):
+        A.check(A.lib().sa2pp_sageattn(C_ref(prob), C_ref(ins), C_ref(qs_struct), qt.workspace.data_ptr(),
+                                       qt.workspace.numel(), C_ref(o), rep_ptr, _stream_ptr(stream)))
+    return (out, qt) if return_quant else out
+
+
+def new_report(device) -> torch.Tensor:
+    """Device RunReport buffer: overflow count, min/max delta_P as float bits (see sa2pp_report)."""
+    r = torch.zeros(4, dtype=torch.int32, device=device)
+    r[1] = 0x7F800000  # +inf bits for the running minimum
+    return r
+
+
+# ----------------------------------------------------------------------------- reference mirror
+@dataclass
+class RunReport:
+    """Mirror of lpattn's RunReport (attention.py:114-125), produced on the GPU."""
+
+    output: np.ndarray
+    overflow_events: int
+    fp16_to_fp32_conversions: int
+    mma_invocations: int
+    p_scale_min: float
+    p_scale_max: float
+    v_scale_min: float
+    v_scale_max: float
+
+
+def _visible(cfg: AttentionConfig, i_stop: int, n_kt: int) -> int:
+    return min(n_kt, -(-i_stop // cfg.block_k)) if cfg.causal else n_kt
+
+
+def _analytic_counts(cfg: AttentionConfig) -> tuple[int, int]:
+    """(fp16->fp32 conversions, mma invocations) exactly as the reference counts them (mma.py:67-86)."""
+    n, d, bq, bk = cfg.seq_len, cfg.head_dim, cfg.block_q, cfg.block_k
+    n_kt = -(-n // bk)
+    conv = mma = 0
+    for i0 in range(0, n, bq):
+        rows = min(bq, n - i0)
+        vis = _visible(cfg, min(i0 + bq, n), n_kt)
+        mma += vis * (rows * bk * (-(-d // MMA_K)) + rows * d * (bk // MMA_K))
+        if cfg.pv_accumulator == "fp16":
+            groups = bk // MMA_K
+            per = -(-groups // cfg.range.buffering_depth)
+            conv += vis * rows * d * per
+    return conv * cfg.num_heads, mma * cfg.num_heads
+
+
+MMA_K = 32
+
+
+def attention_quantized(q, k, v, config: AttentionConfig, *, device: str = "cuda") -> RunReport:
+    """Drop-in for lpattn.attention.attention_quantized (attention.py:232-316), on the B200.
+
+    Accepts (seq, dim) or (heads, seq, dim) arrays like the reference; computes with the
+    sm_100a kernels on float32 copies; returns the output as float64 with the same counters.
+    """
+    if config.head_dim % MMA_K != 0:
+        raise ValueError(f"head_dim must be a multiple of {MMA_K} for the FP8 path")
+    if config.block_k % MMA_K != 0:
+        raise ValueError(f"block_k must be a multiple of {MMA_K} for the FP8 path")
+    if (config.block_q, config.block_k) != (128, 64):
+        raise ValueError("the B200 kernels are built for block_q=128, block_k=64 (reference defaults)")
+    arrs = [np.asarray(t, dtype=np.float64) for t in (q, k, v)]
+    if not (arrs[0].shape == arrs[1].shape == arrs[2].shape):
+        raise ValueError(f"Q/K/V shapes disagree: {arrs[0].shape}, {arrs[1].shape}, {arrs[2].shape}")
+    squeeze = arrs[0].ndim == 2
+    if squeeze:
+        arrs = [a[None] for a in arrs]
+    if arrs[0].ndim != 3:
+        raise ValueError("tensors must be (seq, dim) or (heads, seq, dim)")
+    expected = (config.num_heads, config.seq_len, config.head_dim)
+    if arrs[0].shape != expected:
+        raise ValueError(f"tensor shape {arrs[0].shape} does not match config {expected}")
+    if not all(np.isfinite(a).all() for a in arrs):
+        raise ValueError("Q/K/V must be finite")
+    tq, tk, tv = (torch.from_numpy(a.astype(np.float32))[None].to(device) for a in arrs)
+    rep = new_report(tq.device)
+    out, qt = sageattn(
+        tq, tk, tv, "HND", config.causal, config.scale, pv_accum=config.pv_accumulator,
+        smooth=config.smoothing, qk_bits=config.qk_bits, p_r=config.range.p_r, v_r=config.range.v_r,
+        buffering_depth=config.range.buffering_depth, expect_overflow=config.range.expect_overflow,
+        return_quant=True, report=rep)
+    torch.cuda.synchronize(tq.device)
+    r = rep.cpu().numpy().view(np.uint32)
+    vsc = qt.v_scale64
+    conv, mma = _analytic_counts(config)
+    o = out[0].double().cpu().numpy()
+    return RunReport(
+        output=o[0] if squeeze else o,
+        overflow_events=int(r[0]),
+        fp16_to_fp32_conversions=conv,
+        mma_invocations=mma,
+        p_scale_min=float(np.array([r[1]], dtype=np.uint32).view(np.float32)[0]),
+        p_scale_max=float(np.array([r[2]], dtype=np.uint32).view(np.float32)[0]),
+        v_scale_min=float(vsc.min()),
+        v_scale_max=float(vsc.max()),
+    )
+
+
+def quantize(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, tensor_layout: str = "HND", *,
+             smooth: bool = True, qk_bits: int = 8, v_r: float = 4.5, sm_scale: Optional[float] = None,
+             stream=None) -> QuantizedTensors:
+    """Run only the prepass (smoothing + INT8/E4M3 quantization) and return its tensors."""
+    B, Hq, N, D, qs = _bhnd_view(q, tensor_layout)
+    _, Hkv, _, _, ks = _bhnd_view(k, tensor_layout)
+    _, _, _, _, vs = _bhnd_view(v, tensor_layout)
+    prob = _problem(B, Hq, Hkv, N, D, causal=False, smoothing=smooth, qk_bits=qk_bits, v_r=v_r,
+                    sm_scale=sm_scale)
+    qt = alloc_quant(prob, q.device)
+    ins = A.Inputs(_DT[q.dtype], q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                   (A.C.c_int64 * 3)(*qs), (A.C.c_int64 * 3)(*ks), (A.C.c_int64 * 3)(*vs))
+    qs_struct = qt.struct()
+    with torch.cuda.device(q.device):
+        A.check(A.lib().sa2pp_prepass(C_ref(prob), C_ref(ins), C_ref(qs_struct), qt.workspace.data_ptr(),
+                                      qt.workspace.numel(), _stream_ptr(stream)))
+    return qt
+
+
+def compare(o_ref, o_test):
+    """cossim / relative L1 / RMSE in float64, as lpattn.metrics.compare (metrics.py:33-57)."""
+    a = np.asarray(o_ref, dtype=np.float64).ravel()
+    b = np.asarray(o_test, dtype=np.float64).ravel()
+    if a.shape != b.shape or a.size == 0:
+        raise ValueError("shape mismatch or empty tensors")
+    na, nb, sa = math.sqrt(float(np.sum(a * a))), math.sqrt(float(np.sum(b * b))), float(np.sum(np.abs(a)))
+    if na == 0.0 or sa == 0.0 or nb == 0.0:
+        raise ValueError("degenerate metric denominator")
+    d = a - b
+    return float(np.sum(a * b)) / (na * nb), float(np.sum(np.abs(d))) / sa, math.sqrt(float(np.mean(d * d)))

@@ -1,0 +1,410 @@
+// Fused smoothing + quantization prepass (HBM-bound), sm_100a.
+//
+// Reproduces, bit-exactly, the quantized tensors the reference derives before
+// its tile loop (lpattn attention.py:259-281):
+//   * per-(b,h) FP64 channel means of Q and K            (quantization.py:124-148)
+//   * Q codes: one INT8/INT4 scale per 128-token tile   (quantization.py:151-160, attention.py:279-280)
+//   * K codes: one scale per 64-token block of smoothed, zero-padded K (attention.py:265-273)
+//   * V codes: E4M3, one scale per (64-token block, channel), range v_r (quantization.py:178-188)
+//   * per-key bias b_j = q_mean . Ks_j                   (attention.py:288-289)
+// Arithmetic is FP64 with RNE division, exactly as the reference's numpy float64.
+//
+// Kernels:
+//   channel_sums   grid (chunks, B*(Hq+Hkv))  double-double partial sums over token chunks
+//   channel_means  grid (B*(Hq+Hkv))          fixed-order reduction of the partials -> FP64 mean
+//   quantize_q     grid (nQT, B*Hq)           one CTA per 128-row query tile
+//   quantize_kv    grid (nKB, B*Hkv)          one CTA per 64-key block (K codes, V^T codes, scales, bias)
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "sa2pp_internal.h"
+
+namespace sa2pp {
+
+template <typename T>
+__device__ __forceinline__ double to_f64(T x);
+template <>
+__device__ __forceinline__ double to_f64<float>(float x) { return static_cast<double>(x); }
+template <>
+__device__ __forceinline__ double to_f64<__half>(__half x) { return static_cast<double>(__half2float(x)); }
+template <>
+__device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 x) {
+  return static_cast<double>(__bfloat162float(x));
+}
+
+// Error-free transformation: s + e == a + b exactly.
+__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
+  s = a + b;
+  double bb = s - a;
+  e = (a - (s - bb)) + (b - bb);
+}
+__device__ __forceinline__ void dd_add(double& hi, double& lo, double x) {
+  double s, e;
+  two_sum(hi, x, s, e);
+  lo += e;
+  hi = s;
+}
+
+// Input element (b, h, n, c) with strides in elements; channel dim contiguous.
+struct InView {
+  const void* base;
+  int64_t sb, sh, sn;
+};
+
+template <typename T>
+__device__ __forceinline__ const T* row_ptr(const InView& v, int b, int h, int n) {
+  return static_cast<const T*>(v.base) + b * v.sb + h * v.sh + static_cast<int64_t>(n) * v.sn;
+}
+
+// ------------------------------------------------------------------ pass 1: channel sums
+// blockDim = 256; thread t owns channels [c8*VEC, c8*VEC+VEC) of rows t/(D/VEC) + k*stride.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) channel_sums_kernel(InView qv, InView kv, int Hq, int Hkv, int N,
+                                                           int rows_per_chunk, double2* __restrict__ partial,
+                                                           int n_chunks) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int LANES_PER_ROW = D / VEC;
+  constexpr int ROWS_PER_PASS = 256 / LANES_PER_ROW;
+  const int chunk = blockIdx.x;
+  const int bh = blockIdx.y;  // in [0, B*(Hq+Hkv))
+  const int Ht = Hq + Hkv;
+  const int b = bh / Ht;
+  const int h = bh % Ht;
+  const InView& v = (h < Hq) ? qv : kv;
+  const int hh = (h < Hq) ? h : h - Hq;
+  const int c8 = threadIdx.x % LANES_PER_ROW;
+  const int r0 = threadIdx.x / LANES_PER_ROW;
+  const int n_begin = chunk * rows_per_chunk;
+  const int n_end = min(N, n_begin + rows_per_chunk);
+  double hi[VEC], lo[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) hi[i] = lo[i] = 0.0;
+  for (int n = n_begin + r0; n < n_end; n += ROWS_PER_PASS) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(v, b, hh, n) + c8 * VEC);
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) dd_add(hi[i], lo[i], to_f64<T>(e[i]));
+  }
+  // Fixed-order combine of the ROWS_PER_PASS row-groups through shared memory.
+  __shared__ double2 red[256 * VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) red[threadIdx.x * VEC + i] = make_double2(hi[i], lo[i]);
+  __syncthreads();
+  if (threadIdx.x < LANES_PER_ROW) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      double H = 0.0, L = 0.0;
+      for (int r = 0; r < ROWS_PER_PASS; ++r) {
+        const double2 p = red[(r * LANES_PER_ROW + threadIdx.x) * VEC + i];
+        dd_add(H, L, p.x);
+        L += p.y;
+      }
+      partial[(static_cast<int64_t>(bh) * n_chunks + chunk) * D + threadIdx.x * VEC + i] = make_double2(H, L);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ pass 1b: means
+template <int D>
+__global__ void channel_means_kernel(const double2* __restrict__ partial, int n_chunks, int N,
+                                     double* __restrict__ means) {
+  const int bh = blockIdx.x;
+  for (int c = threadIdx.x; c < D; c += blockDim.x) {
+    double H = 0.0, L = 0.0;
+    for (int k = 0; k < n_chunks; ++k) {
+      const double2 p = partial[(static_cast<int64_t>(bh) * n_chunks + k) * D + c];
+      dd_add(H, L, p.x);
+      L += p.y;
+    }
+    means[static_cast<int64_t>(bh) * D + c] = (H + L) / static_cast<double>(N);
+  }
+}
+
+// ------------------------------------------------------------------ shared helpers
+__device__ __forceinline__ double block_max_256(double x, double* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) scratch[w] = x;
+  __syncthreads();
+  double m = scratch[0];
+#pragma unroll
+  for (int i = 1; i < 8; ++i) m = fmax(m, scratch[i]);
+  return m;
+}
+
+// RNE of x/scale, clipped to +-qmax: the reference's np.clip(np.round(x / scale)).
+__device__ __forceinline__ int quant_int(double x, double scale, int qmax) {
+  double q = rint(__ddiv_rn(x, scale));
+  q = fmin(fmax(q, -static_cast<double>(qmax)), static_cast<double>(qmax));
+  return static_cast<int>(q);
+}
+
+// Direct FP64 -> E4M3 ("fn") with RNE and saturation to +-448 (numerics.py:152-182).
+__device__ __forceinline__ uint8_t e4m3_from_f64(double x) {
+  const uint8_t sign = signbit(x) ? 0x80 : 0x00;
+  const double a = fabs(x);
+  if (a >= 448.0) return sign | 0x7E;
+  if (a < 0.015625) {  // below the smallest normal 2^-6: fixed step 2^-9
+    const double q = rint(a * 512.0);
+    return sign | static_cast<uint8_t>(q);  // q == 8 is exactly the code of 2^-6
+  }
+  int e = ilogb(a);  // floor(log2 a), in [-6, 8]
+  double q = rint(scalbn(a, 3 - e));  // significand * 8 in [8, 16]
+  if (q >= 16.0) {
+    q = 8.0;
+    e += 1;
+  }
+  return sign | static_cast<uint8_t>(((e + 7) << 3) | (static_cast<int>(q) - 8));
+}
+
+// ------------------------------------------------------------------ pass 2: Q tiles
+// One CTA (256 threads) per 128-row tile of one (b, hq).  Rows >= N are written as zero codes.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) quantize_q_kernel(InView qv, int Hq, int N, int Nq_pad, int n_qt, int qmax,
+                                                         const double* __restrict__ means, int Ht,
+                                                         int8_t* __restrict__ q_codes, float* __restrict__ q_scale,
+                                                         double* __restrict__ q_scale64) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int LANES_PER_ROW = D / VEC;
+  constexpr int ROWS_PER_PASS = 256 / LANES_PER_ROW;
+  __shared__ double scratch[8];
+  const int qt = blockIdx.x;
+  const int bh = blockIdx.y;
+  const int b = bh / Hq, h = bh % Hq;
+  const int c8 = threadIdx.x % LANES_PER_ROW;
+  const int r0 = threadIdx.x / LANES_PER_ROW;
+  const int n0 = qt * 128;
+  const int n1 = min(N, n0 + 128);
+  double mu[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) mu[i] = means[(static_cast<int64_t>(b) * Ht + h) * D + c8 * VEC + i];
+  double amax = 0.0;
+  for (int n = n0 + r0; n < n1; n += ROWS_PER_PASS) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(qv, b, h, n) + c8 * VEC);
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) amax = fmax(amax, fabs(to_f64<T>(e[i]) - mu[i]));
+  }
+  amax = block_max_256(amax, scratch);
+  const double scale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
+  if (threadIdx.x == 0) {
+    q_scale[static_cast<int64_t>(bh) * n_qt + qt] = static_cast<float>(scale);
+    q_scale64[static_cast<int64_t>(bh) * n_qt + qt] = scale;
+  }
+  int8_t* dst = q_codes + (static_cast<int64_t>(bh) * Nq_pad) * D;
+  for (int n = n0 + r0; n < n0 + 128; n += ROWS_PER_PASS) {
+    int8_t codes[VEC];
+    if (n < n1) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(qv, b, h, n) + c8 * VEC);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) codes[i] = static_cast<int8_t>(quant_int(to_f64<T>(e[i]) - mu[i], scale, qmax));
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) codes[i] = 0;
+    }
+    int8_t* o = dst + static_cast<int64_t>(n) * D + c8 * VEC;
+    if constexpr (VEC == 8) {
+      *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(codes);
+    } else {
+      *reinterpret_cast<uint32_t*>(o) = *reinterpret_cast<const uint32_t*>(codes);
+    }
+  }
+}
+
+template <int D>
+__host__ __device__ constexpr int kv_smem_ks_bytes() { return 64 * (D + 1) * 8; }
+template <typename T, int D>
+__host__ __device__ constexpr int kv_smem_bytes() {
+  return kv_smem_ks_bytes<D>() + (256 / (D / (16 / sizeof(T)))) * D * 8 + D * 80 + D * 8;
+}
+
+// ------------------------------------------------------------------ pass 3: K/V blocks
+// One CTA (256 threads) per 64-key block of one (b, hkv).
+//   k_codes  [B, Hkv, Np, D]          int8
+//   v_codes  [B, Hkv, D, Np]          E4M3, transposed so the PV operand is K-major
+//   kv_meta  [B, Hkv, nKB, 4 + D]     f32 {dK, 0, 0, 0, dV[0..D)}
+//   bias     [B, Hq, Np]              f32 q_mean . Ks_j ; bias_l2 = bias * sm_scale * log2(e)
+template <typename T, int D>
+__global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v_in, int Hq, int Hkv, int N, int Np,
+                                                          int n_kb, int qmax, double v_r, int smoothing,
+                                                          double sm_scale_log2, const double* __restrict__ means,
+                                                          int Ht, int8_t* __restrict__ k_codes,
+                                                          uint8_t* __restrict__ v_codes, float* __restrict__ kv_meta,
+                                                          double* __restrict__ kv_scale64, float* __restrict__ bias,
+                                                          float* __restrict__ bias_l2) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int LANES_PER_ROW = D / VEC;
+  constexpr int ROWS_PER_PASS = 256 / LANES_PER_ROW;
+  __shared__ double scratch[8];
+  extern __shared__ __align__(16) unsigned char kv_smem[];
+  auto ks = reinterpret_cast<double(*)[D + 1]>(kv_smem);                          // smoothed K rows (FP64)
+  auto vmax_part = reinterpret_cast<double(*)[D]>(kv_smem + kv_smem_ks_bytes<D>());  // per-pass V maxima
+  auto vt = reinterpret_cast<uint8_t(*)[80]>(kv_smem + kv_smem_ks_bytes<D>() + ROWS_PER_PASS * D * 8);
+  double* qmu = reinterpret_cast<double*>(kv_smem + kv_smem_ks_bytes<D>() + ROWS_PER_PASS * D * 8 + D * 80);
+  const int kb = blockIdx.x;
+  const int bh = blockIdx.y;
+  const int b = bh / Hkv, h = bh % Hkv;
+  const int c8 = threadIdx.x % LANES_PER_ROW;
+  const int r0 = threadIdx.x / LANES_PER_ROW;
+  const int n0 = kb * 64;
+  const int n1 = min(N, n0 + 64);
+  double kmu[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) kmu[i] = means[(static_cast<int64_t>(b) * Ht + Hq + h) * D + c8 * VEC + i];
+
+  // ---- K: smoothed values, block amax
+  double amax = 0.0;
+  for (int r = r0; r < 64; r += ROWS_PER_PASS) {
+    const int n = n0 + r;
+    if (n < n1) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(kv_in, b, h, n) + c8 * VEC);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        const double x = to_f64<T>(e[i]) - kmu[i];
+        ks[r][c8 * VEC + i] = x;
+        amax = fmax(amax, fabs(x));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) ks[r][c8 * VEC + i] = 0.0;  // zero padding after smoothing
+    }
+  }
+  amax = block_max_256(amax, scratch);  // also orders the ks[] writes
+  const double kscale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
+  int8_t* kdst = k_codes + (static_cast<int64_t>(bh) * Np + n0) * D;
+  for (int r = r0; r < 64; r += ROWS_PER_PASS) {
+    int8_t codes[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) codes[i] = static_cast<int8_t>(quant_int(ks[r][c8 * VEC + i], kscale, qmax));
+    int8_t* o = kdst + static_cast<int64_t>(r) * D + c8 * VEC;
+    if constexpr (VEC == 8) {
+      *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(codes);
+    } else {
+      *reinterpret_cast<uint32_t*>(o) = *reinterpret_cast<const uint32_t*>(codes);
+    }
+  }
+
+  // ---- V: per-channel block max, codes, transpose
+  double vreg[64 / ROWS_PER_PASS][VEC];
+  double cmax[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) cmax[i] = 0.0;
+#pragma unroll
+  for (int k = 0; k < 64 / ROWS_PER_PASS; ++k) {
+    const int n = n0 + r0 + k * ROWS_PER_PASS;
+    if (n < n1) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(v_in, b, h, n) + c8 * VEC);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        vreg[k][i] = to_f64<T>(e[i]);
+        cmax[i] = fmax(cmax[i], fabs(vreg[k][i]));
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) vreg[k][i] = 0.0;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) vmax_part[r0][c8 * VEC + i] = cmax[i];
+  if (threadIdx.x < D) qmu[threadIdx.x] = 0.0;
+  __syncthreads();
+  float* meta = kv_meta + (static_cast<int64_t>(bh) * n_kb + kb) * (4 + D);
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    double m = 0.0;
+    for (int r = 0; r < ROWS_PER_PASS; ++r) m = fmax(m, vmax_part[r][c8 * VEC + i]);
+    cmax[i] = m > 0.0 ? m / v_r : 1.0;  // now the channel scale
+  }
+  if (r0 == 0) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      meta[4 + c8 * VEC + i] = static_cast<float>(cmax[i]);
+      kv_scale64[(static_cast<int64_t>(bh) * n_kb + kb) * (1 + D) + 1 + c8 * VEC + i] = cmax[i];
+    }
+  }
+  if (threadIdx.x < 4) meta[threadIdx.x] = threadIdx.x == 0 ? static_cast<float>(kscale) : 0.0f;
+  if (threadIdx.x == 0) kv_scale64[(static_cast<int64_t>(bh) * n_kb + kb) * (1 + D)] = kscale;
+#pragma unroll
+  for (int k = 0; k < 64 / ROWS_PER_PASS; ++k) {
+    const int r = r0 + k * ROWS_PER_PASS;
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) vt[c8 * VEC + i][r] = e4m3_from_f64(__ddiv_rn(vreg[k][i], cmax[i]));
+  }
+  __syncthreads();
+  // Each channel row of the transposed tile is 64 contiguous bytes: 4 x 16B per row.
+  uint8_t* vdst = v_codes + static_cast<int64_t>(bh) * D * Np + n0;
+  for (int idx = threadIdx.x; idx < D * 4; idx += 256) {
+    const int c = idx >> 2, part = idx & 3;
+    *reinterpret_cast<uint4*>(vdst + static_cast<int64_t>(c) * Np + part * 16) =
+        *reinterpret_cast<const uint4*>(&vt[c][part * 16]);
+  }
+
+  // ---- bias for every query head sharing this KV head: b_j = q_mean . Ks_j (FP64)
+  const int group = Hq / Hkv;
+  for (int g = 0; g < group; ++g) {
+    const int hq = h * group + g;
+    __syncthreads();
+    if (threadIdx.x < D)
+      qmu[threadIdx.x] = smoothing ? means[(static_cast<int64_t>(b) * Ht + hq) * D + threadIdx.x] : 0.0;
+    __syncthreads();
+    if (threadIdx.x < 64) {
+      const int r = threadIdx.x;
+      double acc = 0.0;
+      for (int c = 0; c < D; ++c) acc = fma(qmu[c], ks[r][c], acc);
+      const int64_t o = (static_cast<int64_t>(b) * Hq + hq) * Np + n0 + r;
+      bias[o] = static_cast<float>(acc);
+      bias_l2[o] = static_cast<float>(acc * sm_scale_log2);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host launcher
+template <typename T, int D>
+static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
+  InView qv{L.q, L.q_stride[0], L.q_stride[1], L.q_stride[2]};
+  InView kv{L.k, L.k_stride[0], L.k_stride[1], L.k_stride[2]};
+  InView vv{L.v, L.v_stride[0], L.v_stride[1], L.v_stride[2]};
+  const int Ht = L.Hq + L.Hkv;
+  if (L.smoothing) {
+    dim3 g1(L.n_chunks, L.B * Ht);
+    channel_sums_kernel<T, D><<<g1, 256, 0, st>>>(qv, kv, L.Hq, L.Hkv, L.N, L.rows_per_chunk, L.partial,
+                                                  L.n_chunks);
+    channel_means_kernel<D><<<L.B * Ht, 128, 0, st>>>(L.partial, L.n_chunks, L.N, L.means);
+  } else {
+    cudaMemsetAsync(L.means, 0, sizeof(double) * L.B * Ht * D, st);
+  }
+  dim3 gq(L.n_qt, L.B * L.Hq);
+  quantize_q_kernel<T, D><<<gq, 256, 0, st>>>(qv, L.Hq, L.N, L.Nq_pad, L.n_qt, L.qmax, L.means, Ht, L.q_codes,
+                                              L.q_scale, L.q_scale64);
+  dim3 gk(L.n_kb, L.B * L.Hkv);
+  constexpr int kv_smem = kv_smem_bytes<T, D>();
+  static bool attr_set = false;  // per template instance; benign race (idempotent)
+  if (!attr_set) {
+    cudaFuncSetAttribute(quantize_kv_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kv_smem);
+    attr_set = true;
+  }
+  quantize_kv_kernel<T, D><<<gk, 256, kv_smem, st>>>(kv, vv, L.Hq, L.Hkv, L.N, L.Np, L.n_kb, L.qmax, L.v_r, L.smoothing,
+                                               L.sm_scale_log2, L.means, Ht, L.k_codes, L.v_codes, L.kv_meta,
+                                               L.kv_scale64, L.bias, L.bias_l2);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_prepass(const PrepassLaunch& L, cudaStream_t st) {
+  switch (L.dtype * 1000 + L.D) {
+    case SA2PP_F32 * 1000 + 64: return launch_prepass_t<float, 64>(L, st);
+    case SA2PP_F32 * 1000 + 128: return launch_prepass_t<float, 128>(L, st);
+    case SA2PP_F16 * 1000 + 64: return launch_prepass_t<__half, 64>(L, st);
+    case SA2PP_F16 * 1000 + 128: return launch_prepass_t<__half, 128>(L, st);
+    case SA2PP_BF16 * 1000 + 64: return launch_prepass_t<__nv_bfloat16, 64>(L, st);
+    case SA2PP_BF16 * 1000 + 128: return launch_prepass_t<__nv_bfloat16, 128>(L, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace sa2pp

@@ -1,0 +1,50 @@
+// Internal launch descriptors shared by the C-ABI layer and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "../../include/sa2pp.h"
+
+namespace sa2pp {
+
+constexpr int kBlockQ = 128;  // attention.py:62
+constexpr int kBlockK = 64;   // attention.py:63
+
+struct PrepassLaunch {
+  int dtype, D, B, Hq, Hkv, N, Nq_pad, Np, n_qt, n_kb, qmax, smoothing;
+  int rows_per_chunk, n_chunks;
+  double v_r, sm_scale_log2;
+  const void *q, *k, *v;
+  int64_t q_stride[3], k_stride[3], v_stride[3];
+  double2* partial;
+  double* means;
+  int8_t* q_codes;
+  float* q_scale;
+  double* q_scale64;
+  int8_t* k_codes;
+  uint8_t* v_codes;
+  float* kv_meta;
+  double* kv_scale64;
+  float* bias;
+  float* bias_l2;
+};
+
+struct AttnParams {
+  int B, Hq, Hkv, N, Nq_pad, Np, n_qt, n_kb, group;
+  int out_dtype;
+  float sm_scale_log2;  // sm_scale * log2(e)
+  float log2_pr;        // log2(p_r)
+  float inv_pr;         // 1 / p_r
+  const float* q_scale;
+  const float* kv_meta;
+  const float* bias_l2;
+  void* out;
+  int64_t o_sb, o_sh, o_sn;
+  sa2pp_report* report;
+  uint32_t* debug;
+};
+
+cudaError_t launch_prepass(const PrepassLaunch& L, cudaStream_t st);
+cudaError_t launch_attn(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st);
+
+}  // namespace sa2pp

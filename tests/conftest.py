@@ -39,3 +39,20 @@ def lpattn():
     sys.path.insert(0, str(REF_SRC))
     import lpattn as mod
     return mod
+
+
+def golden_config(g):
+    """(seq, dim, heads, causal, smoothing, qk_bits, pv, depth, waive, p_r, v_r, sm_scale) of a fixture."""
+    seq, dim, heads, causal, smoothing, qk_bits, fp16, depth, waive = (int(x) for x in g["cfg"])
+    p_r, v_r, sm = (float(x) for x in g["ranges"])
+    return dict(seq=seq, dim=dim, heads=heads, causal=bool(causal), smoothing=bool(smoothing),
+                qk_bits=qk_bits, pv="fp16" if fp16 else "fp32", depth=depth, waive=bool(waive),
+                p_r=p_r, v_r=v_r, sm_scale=None if sm < 0 else sm)
+
+
+def gpu_ready() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False

@@ -1,0 +1,172 @@
+"""Parity of the sm_100a kernels against the reference (golden fixtures) and the CPU oracle.
+
+Bar:
+  * prepass: Q/K INT8 codes, V E4M3 codes, FP64 scales and means BIT-EXACT vs the reference;
+    f32 scales = float32(reference); bias within 1 float32 ulp.
+  * attention output vs the reference's own output: cossim >= 0.9999 and relative L1 <= 1e-3
+    (fp32 output), <= 3e-3 for bf16 output;  vs FP64 exact attention: cossim >= 0.999 and
+    L1 <= (reference's own L1 vs exact) + 1e-3.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, golden_config, gpu_ready, load_golden
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not gpu_ready():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2505_21136_b200 as sa  # noqa: E402
+from oracle import sage_cpu as oc  # noqa: E402
+
+SUPPORTED = [n for n in golden_cases()
+             if golden_config(load_golden(n))["dim"] in (64, 128)
+             and not (golden_config(load_golden(n))["pv"] == "fp16" and golden_config(load_golden(n))["depth"] == 1)]
+
+
+def run_case(g, dtype=torch.float32, layout="HND"):
+    c = golden_config(g)
+    q, k, v = (torch.from_numpy(g[x]).to("cuda", dtype)[None] for x in ("q", "k", "v"))
+    if layout == "NHD":
+        q, k, v = (t.transpose(1, 2).contiguous() for t in (q, k, v))
+    rep = sa.new_report("cuda")
+    out, qt = sa.sageattn(q, k, v, layout, c["causal"], c["sm_scale"], pv_accum=c["pv"],
+                          smooth=c["smoothing"], qk_bits=c["qk_bits"], p_r=c["p_r"], v_r=c["v_r"],
+                          buffering_depth=c["depth"], expect_overflow=c["waive"], return_quant=True,
+                          report=rep)
+    torch.cuda.synchronize()
+    if layout == "NHD":
+        out = out.transpose(1, 2)
+    return out[0].double().cpu().numpy(), qt, rep.cpu().numpy().view(np.uint32)
+
+
+def f32_ulp_close(a32, b64):
+    b32 = b64.astype(np.float32)
+    ulp = np.spacing(np.abs(b32)).astype(np.float64)
+    return np.all(np.abs(a32.astype(np.float64) - b32.astype(np.float64)) <= ulp + 1e-30)
+
+
+@pytest.mark.parametrize("name", SUPPORTED)
+def test_prepass_bit_exact(name):
+    g = load_golden(name)
+    c = golden_config(g)
+    n = c["seq"]
+    _, qt, _ = run_case(g)
+    qc = qt.q_codes[0].cpu().numpy()
+    assert np.array_equal(qc[:, :n], g["q_codes"]), "Q INT8 codes"
+    assert not qc[:, n:].any(), "Q pad rows must be zero"
+    assert np.array_equal(qt.q_scale64[0].cpu().numpy(), g["q_scale"]), "Q scales (f64)"
+    assert np.array_equal(qt.q_scale[0].cpu().numpy(), g["q_scale"].astype(np.float32)), "Q scales (f32)"
+    assert np.array_equal(qt.k_codes[0].cpu().numpy(), g["k_codes"]), "K INT8 codes"
+    assert np.array_equal(qt.k_scale64[0].cpu().numpy(), g["k_scale"]), "K scales"
+    vt = qt.v_codes[0].cpu().numpy().transpose(0, 2, 1)
+    assert np.array_equal(vt, g["v_codes"]), "V E4M3 codes"
+    assert np.array_equal(qt.v_scale64[0].cpu().numpy(), g["v_scale"]), "V scales"
+    means = qt.means[0].cpu().numpy()
+    assert np.array_equal(means[: c["heads"]], g["q_mean"]), "Q means"
+    assert np.array_equal(means[c["heads"]:], g["k_mean"]), "K means"
+    assert f32_ulp_close(qt.bias[0].cpu().numpy(), g["bias"]), "bias within 1 ulp f32"
+
+
+@pytest.mark.parametrize("name", SUPPORTED)
+def test_output_vs_reference(name):
+    g = load_golden(name)
+    out, _, rep = run_case(g)
+    cos, l1, _ = sa.compare(g["out"], out)
+    assert cos >= 0.9999 and l1 <= 1e-3, (cos, l1)
+    cos_x, l1_x, _ = sa.compare(g["out_exact"], out)
+    _, l1_ref, _ = sa.compare(g["out_exact"], g["out"])
+    assert cos_x >= 0.999 and l1_x <= l1_ref + 1e-3, (cos_x, l1_x, l1_ref)
+    assert rep[0] == int(g["overflow"])
+
+
+@pytest.mark.parametrize("name", ["attn_bf16_d128", "attn_bf16_causal_d64"])
+def test_bf16_inputs_bit_exact_and_close(name):
+    g = load_golden(name)  # inputs are bf16-representable, so bf16 tensors carry them exactly
+    out, qt, _ = run_case(g, dtype=torch.bfloat16)
+    n = golden_config(g)["seq"]
+    assert np.array_equal(qt.q_codes[0].cpu().numpy()[:, :n], g["q_codes"])
+    assert np.array_equal(qt.v_codes[0].cpu().numpy().transpose(0, 2, 1), g["v_codes"])
+    cos, l1, _ = sa.compare(g["out"], out)
+    assert cos >= 0.9999 and l1 <= 3e-3, (cos, l1)
+
+
+def test_nhd_layout_matches_hnd():
+    g = load_golden("attn_ragged_voffset_d64")
+    a, _, _ = run_case(g, layout="HND")
+    b, _, _ = run_case(g, layout="NHD")
+    assert np.array_equal(a, b)
+
+
+def test_deterministic():
+    g = load_golden("attn_uniform_d128")
+    a, _, _ = run_case(g)
+    b, _, _ = run_case(g)
+    assert np.array_equal(a, b)
+
+
+def test_qk_scores_exact_in_tmem():
+    """The INT8 tcgen05 MMA result (TMEM dump of block 0) equals the exact integer product."""
+    g = load_golden("attn_bf16_d128")
+    dbg = torch.zeros(128 * (64 + 128), dtype=torch.int32, device="cuda")
+    sa._abi.lib().sa2pp_set_debug_buffer(dbg.data_ptr())
+    try:
+        run_case(g)
+    finally:
+        sa._abi.lib().sa2pp_set_debug_buffer(None)
+    s = dbg[: 128 * 64].view(128, 64).cpu().numpy().astype(np.int64)
+    want = g["q_codes"][0][:128].astype(np.int64) @ g["k_codes"][0][:64].astype(np.int64).T
+    assert np.array_equal(s, want)
+
+
+def test_reference_mirror_run_report():
+    g = load_golden("attn_oracle")
+    c = golden_config(g)
+    cfg = sa.AttentionConfig(seq_len=c["seq"], head_dim=c["dim"], num_heads=c["heads"])
+    rep = sa.attention_quantized(g["q"], g["k"], g["v"], cfg)
+    assert rep.mma_invocations == int(g["mma"])
+    assert rep.fp16_to_fp32_conversions == int(g["conversions"])
+    assert rep.overflow_events == 0
+    assert rep.p_scale_max <= 1.0 / 224.0 * (1 + 1e-6)
+    assert rep.v_scale_min == float(g["v_scale_min"]) and rep.v_scale_max == float(g["v_scale_max"])
+    cos, l1, _ = sa.compare(g["out"], rep.output)
+    assert cos >= 0.9999 and l1 <= 1e-3
+
+
+def test_gqa_equals_repeated_kv_heads():
+    rng = np.random.default_rng(5)
+    q = torch.from_numpy(rng.normal(size=(1, 8, 300, 128)).astype(np.float32)).cuda()
+    k = torch.from_numpy(rng.normal(size=(1, 2, 300, 128)).astype(np.float32)).cuda()
+    v = torch.from_numpy(rng.normal(size=(1, 2, 300, 128)).astype(np.float32)).cuda()
+    a = sa.sageattn(q, k, v, is_causal=True)
+    b = sa.sageattn(q, k.repeat_interleave(4, 1), v.repeat_interleave(4, 1), is_causal=True)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+@pytest.mark.parametrize("n", [1000, 4096])
+def test_large_vs_exact_attention(causal, n):
+    """Bench-shaped bf16 inputs (V with channel offsets): property check vs FP32 SDPA."""
+    g = torch.Generator(device="cuda").manual_seed(n + causal)
+    q = torch.randn(2, 4, n, 128, device="cuda", generator=g).bfloat16()
+    k = torch.randn(2, 4, n, 128, device="cuda", generator=g).bfloat16()
+    v = (torch.randn(2, 4, n, 128, device="cuda", generator=g)
+         + 2 * torch.randn(2, 4, 1, 128, device="cuda", generator=g)).bfloat16()
+    o = sa.sageattn(q, k, v, is_causal=causal)
+    ref = torch.nn.functional.scaled_dot_product_attention(q.float(), k.float(), v.float(), is_causal=causal)
+    cos, l1, _ = sa.compare(ref.cpu().numpy(), o.float().cpu().numpy())
+    assert cos >= 0.999 and l1 <= 2e-2, (cos, l1)
+
+
+def test_fp32_accumulator_close_to_fp16():
+    g = load_golden("attn_bf16_d128")
+    c = golden_config(g)
+    q, k, v = (torch.from_numpy(g[x]).cuda()[None] for x in ("q", "k", "v"))
+    a = sa.sageattn(q, k, v, pv_accum="fp16").cpu().numpy()
+    b = sa.sageattn(q, k, v, pv_accum="fp32").cpu().numpy()
+    cos, l1, _ = sa.compare(a, b)
+    assert cos >= 0.9999 and l1 <= 1e-3
