@@ -78,8 +78,9 @@ def test_output_vs_reference(name):
     cos, l1, _ = sa.compare(g["out"], out)
     assert cos >= 0.9999 and l1 <= 1e-3, (cos, l1)
     cos_x, l1_x, _ = sa.compare(g["out_exact"], out)
-    _, l1_ref, _ = sa.compare(g["out_exact"], g["out"])
-    assert cos_x >= 0.999 and l1_x <= l1_ref + 1e-3, (cos_x, l1_x, l1_ref)
+    cos_ref, l1_ref, _ = sa.compare(g["out_exact"], g["out"])
+    # the reference's own accuracy vs exact sets the bar (INT4 mode is far below 0.999 itself)
+    assert cos_x >= min(0.999, cos_ref - 1e-4) and l1_x <= l1_ref + 1e-3, (cos_x, l1_x, cos_ref, l1_ref)
     assert rep[0] == int(g["overflow"])
 
 

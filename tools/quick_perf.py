@@ -1,5 +1,7 @@
 """Quick device timing of prepass and attention kernels (development aid, not the bench)."""
 import sys
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_2505_21136_b200 as sa
 from paper_2505_21136_b200 import api, _abi as A
