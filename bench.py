@@ -1,0 +1,349 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SageAttention2++ path (BASELINE.json metric: attention TOPS).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--seq 16384] [--causal] [--pv-accum fp16|fp32]
+
+Workload (BASELINE.json configs[1], the headline): kernel bench, batch 4, 32 heads,
+head_dim 128, seq 16384, non-causal, bf16 Q/K/V (synthetic N(0,1)).  A step is one
+sageattn forward (prepass + attention kernel) over the whole batch.  Metric: attention
+TOPS = 4*B*H*N^2*D (x0.5 causal) / time.  Multi-GPU: the 128 (batch, head) units are
+sharded across ranks with no data-path collective (strong scaling); value = all ranks'
+ops / max-over-ranks device time.  Rank 0 prints ONE JSON line.
+
+--impl reference times the reference's CPU path (the numpy restatement of lpattn in
+oracle/sage_cpu.py, all host cores, one head per process) on a bounded sample of the
+same workload; the reference itself is pure Python and cannot travel to the GPU box.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+B_DEFAULT, H_DEFAULT, D_DEFAULT = 4, 32, 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--batch", type=int, default=B_DEFAULT)
+    ap.add_argument("--heads", type=int, default=H_DEFAULT)
+    ap.add_argument("--seq", type=int, default=16384)
+    ap.add_argument("--head-dim", type=int, default=D_DEFAULT)
+    ap.add_argument("--causal", action="store_true")
+    ap.add_argument("--pv-accum", choices=["fp16", "fp32"], default="fp16")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def ops_of(B, H, N, D, causal):
+    return 4.0 * B * H * N * N * D * (0.5 if causal else 1.0)
+
+
+def workload_name(a):
+    return (f"kernel_bench_b{a.batch}_h{a.heads}_n{a.seq}_d{a.head_dim}_"
+            f"{'causal' if a.causal else 'noncausal'}")
+
+
+def metric_name():
+    return "attention TOPS (hd128, seq 1K-32K, causal/non-causal) vs B200 FP8 peak; cossim/L1"
+
+
+# ----------------------------------------------------------------------------- CPU reference leg
+def _cpu_head(args):
+    seed, n, d, causal = args
+    import numpy as np
+    from oracle import sage_cpu as oc
+    rng = np.random.Generator(np.random.Philox(seed))
+    q, k, v = (rng.normal(size=(n, d)).astype(np.float32) for _ in range(3))
+    cfg = oc.AttentionConfig(seq_len=n, head_dim=d, causal=causal)
+    t0 = time.perf_counter()
+    oc.attention_quantized(q, k, v, cfg)
+    return time.perf_counter() - t0
+
+
+def cpu_reference_rate(n_sample: int, d: int, causal: bool, procs: int):
+    """Reference CPU path on `procs` heads of (n_sample x d) in parallel; returns (TOPS, wall s)."""
+    import concurrent.futures as cf
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    t0 = time.perf_counter()
+    with cf.ProcessPoolExecutor(procs) as ex:
+        list(ex.map(_cpu_head, [(1000 + i, n_sample, d, causal) for i in range(procs)]))
+    wall = time.perf_counter() - t0
+    return procs * ops_of(1, 1, n_sample, d, causal) / wall / 1e12, wall
+
+
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    procs = max(1, os.cpu_count() or 1)
+    n_sample = 1024
+    vals = []
+    for i in range(a.warmup + a.steps):
+        v, _ = cpu_reference_rate(n_sample, a.head_dim, a.causal, procs) if i >= a.warmup else (None, None)
+        if i >= a.warmup:
+            vals.append(v)
+        elif i == 0:
+            cpu_reference_rate(256, a.head_dim, a.causal, procs)  # warm the pool/imports once
+    value = statistics.median(vals)
+    sample = (f"{procs} heads x seq {n_sample} x d {a.head_dim} "
+              f"{'causal' if a.causal else 'non-causal'}, fp32 N(0,1), one head per process")
+    line = {
+        "impl": "reference", "metric": metric_name(), "value": value, "unit": "TOPS",
+        "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ops_of(1, procs, n_sample, a.head_dim, a.causal) / (value * 1e12) * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64 (numpy emulation of int8/e4m3/fp16-acc)", "data": "synthetic",
+        "config": {"workload": workload_name(a), "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "TOPS", "cores": procs, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU leg
+class ClockSampler:
+    def __init__(self, idx: int):
+        self.idx = idx
+        self.proc = None
+        self.path = Path(f"/tmp/sa2pp_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if self.proc is None or not self.path.exists():
+            return None
+        rows = []
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                try:
+                    rows.append((float(parts[0]), float(parts[1]), parts[4:8]))
+                except ValueError:
+                    pass
+        if not rows:
+            return None
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, x in enumerate(r) if x.lower() == "active"})
+        loaded = [c for c, _, _ in rows if c > 500] or [c for c, _, _ in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(m for _, m, _ in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def read_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("bf16_tflops", 1590.0)), "MEASURED_PEAKS.json"
+    return 1590.0, "fallback (B200_PROFILING.md)"
+
+
+def read_traffic(workload: str):
+    p = ROOT / "profiles" / "attn_ncu_summary.json"
+    if not p.exists():
+        return None
+    d = json.loads(p.read_text())
+    e = d.get(workload)
+    return None if e is None else e.get("dram_bytes_per_launch")
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    import paper_2505_21136_b200 as sa
+    from paper_2505_21136_b200 import api, _abi as A
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    B, H, N, D = a.batch, a.heads, a.seq, a.head_dim
+    # shard the (batch, head) units across ranks: heads split evenly (no collective on the data path)
+    units = B * H
+    if units % world:
+        raise SystemExit(f"{units} (batch, head) units do not divide over {world} ranks")
+    Bl, Hl = (B, H // world) if H % world == 0 else (B // world, H)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    q = torch.randn(Bl, Hl, N, D, device=dev, generator=gen, dtype=torch.float32).bfloat16()
+    k = torch.randn(Bl, Hl, N, D, device=dev, generator=gen, dtype=torch.float32).bfloat16()
+    v = torch.randn(Bl, Hl, N, D, device=dev, generator=gen, dtype=torch.float32).bfloat16()
+    out = torch.empty_like(q)
+    prob = api._problem(Bl, Hl, Hl, N, D, causal=a.causal, pv_accum=a.pv_accum)
+    qt = api.alloc_quant(prob, dev)
+    import ctypes
+    stream = torch.cuda.current_stream(dev)
+    sp = stream.cuda_stream
+    ins = A.Inputs(A.SA2PP_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                   (ctypes.c_int64 * 3)(q.stride(0), q.stride(1), q.stride(2)),
+                   (ctypes.c_int64 * 3)(k.stride(0), k.stride(1), k.stride(2)),
+                   (ctypes.c_int64 * 3)(v.stride(0), v.stride(1), v.stride(2)))
+    o = A.Output(A.SA2PP_BF16, out.data_ptr(), (ctypes.c_int64 * 3)(out.stride(0), out.stride(1), out.stride(2)))
+    qs = qt.struct()
+    lib = A.lib()
+
+    def prepass():
+        A.check(lib.sa2pp_prepass(ctypes.byref(prob), ctypes.byref(ins), ctypes.byref(qs),
+                                  qt.workspace.data_ptr(), qt.workspace.numel(), sp))
+
+    def attn():
+        A.check(lib.sa2pp_attn_fwd(ctypes.byref(prob), ctypes.byref(qs), ctypes.byref(o), None, sp))
+
+    launches_per_step = 5  # channel_sums, channel_means, quantize_q, quantize_kv, attn_fwd
+
+    for _ in range(a.warmup):
+        prepass()
+        attn()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        for e0, e1, e2 in ev:
+            e0.record(stream)
+            prepass()
+            e1.record(stream)
+            attn()
+            e2.record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    total_ms = t_start.elapsed_time(t_end)
+    attn_ms = statistics.mean(e1.elapsed_time(e2) for _, e1, e2 in ev)
+    pre_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1, _ in ev)
+    if world > 1:
+        t = torch.tensor([total_ms, attn_ms, pre_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, attn_ms, pre_ms = t.tolist()
+    ms_per_step = total_ms / a.steps
+    job_ops = ops_of(B, H, N, D, a.causal)
+    value = job_ops / (ms_per_step * 1e-3) / 1e12
+
+    # ---------------- end-to-end through the public API with pinned host buffers
+    e2e = None
+    if not a.no_e2e:
+        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
+        ho = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+
+        def e2e_step():
+            dq, dk, dv = (h.to(dev, non_blocking=True) for h in (hq, hk, hv))
+            r = sa.sageattn(dq, dk, dv, "HND", a.causal, None, pv_accum=a.pv_accum, quant=qt, out=out)
+            ho.copy_(r, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_e2e = max(1, min(a.steps, 5))
+        s0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        s1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = s0.elapsed_time(s1) / n_e2e
+        if world > 1:
+            t = torch.tensor([e2e_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_ms = t.item()
+        e2e = {"value": job_ops / (e2e_ms * 1e-3) / 1e12, "unit": "TOPS",
+               "h2d_bytes_per_step": 3 * q.numel() * q.element_size() * world,
+               "d2h_bytes_per_step": out.numel() * out.element_size() * world,
+               "ms_per_step": e2e_ms}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    bf16_peak, peak_src = read_peaks()
+    fp8_peak = 2.0 * bf16_peak  # dense FP8/INT8 tensor rate is 2x dense BF16 on B200
+    attn_ops_per_launch = ops_of(Bl, Hl, N, D, a.causal)
+    achieved = attn_ops_per_launch / (attn_ms * 1e-3) / 1e12
+    line = {
+        "metric": metric_name(), "value": value, "unit": "TOPS", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "int8 QK / e4m3 PV (fp16 acc)" if a.pv_accum == "fp16" else "int8 QK / e4m3 PV (fp32 acc)",
+        "data": "synthetic N(0,1) bf16 Q/K/V",
+        "config": {"workload": workload_name(a), "batch": B, "heads": H, "seq_len": N, "head_dim": D,
+                   "causal": a.causal, "pv_accum": a.pv_accum, "parallelism": f"bh-shard x{world}",
+                   "l2": "inputs larger than L2 (3 x %.0f MB bf16 per GPU)" % (q.numel() * 2 / 1e6)},
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
+                     "frac": achieved / fp8_peak, "traffic": read_traffic(workload_name(a)),
+                     "kernel": "attn_fwd_kernel", "ops_per_launch": attn_ops_per_launch,
+                     "ms_per_launch": attn_ms, "peak_source": f"2 x bf16 {bf16_peak} ({peak_src})",
+                     "frac_of_nominal_4500": achieved / 4500.0},
+        "prepass": {"ms_per_launch": pre_ms, "hbm_bytes": 13 * Bl * Hl * N * D,
+                    "achieved_gbs": 13 * Bl * Hl * N * D / (pre_ms * 1e-3) / 1e9},
+        "gpu_launches": launches_per_step * a.steps,
+        "clocks": clk.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if not a.no_cpu:
+        procs = max(1, os.cpu_count() or 1)
+        v_cpu, wall = cpu_reference_rate(1024, D, a.causal, procs)
+        line["cpu_baseline"] = {"value": v_cpu, "unit": "TOPS", "cores": procs, "kind": "port",
+                                "sample": f"{procs} heads x seq 1024 x d {D}, one head per process "
+                                          f"({wall:.1f} s wall); rate is N-independent (SURVEY A.8)"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = parse()
+    if a.warmup < 3:
+        a.warmup = 3
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()
