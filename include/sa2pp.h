@@ -154,6 +154,10 @@ SA2PP_API int sa2pp_sageattn(const sa2pp_problem* prob, const sa2pp_inputs* in, 
  * Set to NULL to disable.  Used by the parity tests to localise failures. */
 SA2PP_API int sa2pp_set_debug_buffer(void* dbg);
 
+/* Development aid: per-phase clock64 trace of the CTAs of (batch 0, head 0) with query tile < 8,
+ * written as uint64 [8][66][8] (see tools/trace_phases.py).  NULL disables. */
+SA2PP_API int sa2pp_set_trace_buffer(void* buf);
+
 #ifdef __cplusplus
 }
 #endif

@@ -19,6 +19,7 @@ SA2PP_ACC_F16, SA2PP_ACC_F32 = range(2)
 EXPORTED = (
     "sa2pp_version", "sa2pp_last_error", "sa2pp_check_problem", "sa2pp_quant_sizes",
     "sa2pp_prepass", "sa2pp_attn_fwd", "sa2pp_sageattn", "sa2pp_set_debug_buffer",
+    "sa2pp_set_trace_buffer",
 )
 
 
@@ -82,6 +83,7 @@ def lib() -> C.CDLL:
         h.sa2pp_sageattn.argtypes = [P(Problem), P(Inputs), P(Quant), C.c_void_p, C.c_size_t,
                                      P(Output), C.c_void_p, C.c_void_p]
         h.sa2pp_set_debug_buffer.argtypes = [C.c_void_p]
+        h.sa2pp_set_trace_buffer.argtypes = [C.c_void_p]
         for name in EXPORTED[2:]:
             getattr(h, name).restype = C.c_int
         _lib = h

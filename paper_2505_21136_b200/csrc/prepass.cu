@@ -215,19 +215,43 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(InView qv, int Hq, int 
   }
 }
 
-template <int D>
-__host__ __device__ constexpr int kv_smem_ks_bytes() { return 64 * (D + 1) * 8; }
-template <typename T, int D>
-__host__ __device__ constexpr int kv_smem_bytes() {
-  return kv_smem_ks_bytes<D>() + (256 / (D / (16 / sizeof(T)))) * D * 8 + D * 80 + D * 8;
+// x / scale rounded to nearest-even, bit-identical to the FP64 division the reference does
+// (np.round(x / scale)): multiply by the reciprocal and fall back to the correctly rounded
+// division only when the product lies within 1e-9 of a rounding tie.
+__device__ __forceinline__ double div_rint(double x, double scale, double inv) {
+  double q = x * inv;
+  const double fr = fabs(q - trunc(q));
+  if (fabs(fr - 0.5) < 1e-9) q = __ddiv_rn(x, scale);
+  return rint(q);
+}
+
+// E4M3 code of x / scale, bit-identical to encoding the correctly rounded FP64 quotient: the
+// reciprocal product is used unless it sits within 1e-9 (relative to the grid step) of an E4M3
+// rounding boundary, in which case the exact quotient is encoded.
+__device__ __forceinline__ uint8_t e4m3_div(double x, double scale, double inv) {
+  double q = x * inv;
+  const double a = fabs(q);
+  if (a < 448.0) {
+    const int e = a < 0.015625 ? -6 : ilogb(a);
+    const double m = scalbn(a, 3 - e);  // grid units: ties sit at k + 0.5
+    const double fr = m - trunc(m);
+    if (fabs(fr - 0.5) < 1e-9) q = __ddiv_rn(x, scale);
+  }
+  return e4m3_from_f64(q);
 }
 
 // ------------------------------------------------------------------ pass 3: K/V blocks
-// One CTA (256 threads) per 64-key block of one (b, hkv).
+// One CTA (256 threads) per 64-key block of one (b, hkv).  The raw K and V tiles are staged in
+// shared memory once; everything else works from there.
 //   k_codes  [B, Hkv, Np, D]          int8
 //   v_codes  [B, Hkv, D, Np]          E4M3, transposed so the PV operand is K-major
 //   kv_meta  [B, Hkv, nKB, 4 + D]     f32 {dK, 0, 0, 0, dV[0..D)}
 //   bias     [B, Hq, Np]              f32 q_mean . Ks_j ; bias_l2 = bias * sm_scale * log2(e)
+template <typename T, int D>
+__host__ __device__ constexpr int kv_smem_bytes() {
+  return 2 * 64 * D * static_cast<int>(sizeof(T)) + 3 * D * 8 + 64;
+}
+
 template <typename T, int D>
 __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v_in, int Hq, int Hkv, int N, int Np,
                                                           int n_kb, int qmax, double v_r, int smoothing,
@@ -237,126 +261,114 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v
                                                           double* __restrict__ kv_scale64, float* __restrict__ bias,
                                                           float* __restrict__ bias_l2) {
   constexpr int VEC = 16 / sizeof(T);
-  constexpr int LANES_PER_ROW = D / VEC;
-  constexpr int ROWS_PER_PASS = 256 / LANES_PER_ROW;
-  __shared__ double scratch[8];
+  constexpr int NV = 64 * D / VEC;  // 16-byte vectors per tile
   extern __shared__ __align__(16) unsigned char kv_smem[];
-  auto ks = reinterpret_cast<double(*)[D + 1]>(kv_smem);                          // smoothed K rows (FP64)
-  auto vmax_part = reinterpret_cast<double(*)[D]>(kv_smem + kv_smem_ks_bytes<D>());  // per-pass V maxima
-  auto vt = reinterpret_cast<uint8_t(*)[80]>(kv_smem + kv_smem_ks_bytes<D>() + ROWS_PER_PASS * D * 8);
-  double* qmu = reinterpret_cast<double*>(kv_smem + kv_smem_ks_bytes<D>() + ROWS_PER_PASS * D * 8 + D * 80);
+  T* kraw = reinterpret_cast<T*>(kv_smem);
+  T* vraw = kraw + 64 * D;
+  double* kmu = reinterpret_cast<double*>(kv_smem + 2 * 64 * D * sizeof(T));
+  double* qmu = kmu + D;
+  double* vsc = qmu + D;
+  __shared__ double scratch[8];
   const int kb = blockIdx.x;
   const int bh = blockIdx.y;
   const int b = bh / Hkv, h = bh % Hkv;
-  const int c8 = threadIdx.x % LANES_PER_ROW;
-  const int r0 = threadIdx.x / LANES_PER_ROW;
   const int n0 = kb * 64;
-  const int n1 = min(N, n0 + 64);
-  double kmu[VEC];
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) kmu[i] = means[(static_cast<int64_t>(b) * Ht + Hq + h) * D + c8 * VEC + i];
+  const int rows = min(64, N - n0);
+  const int tid = threadIdx.x;
 
-  // ---- K: smoothed values, block amax
+  // ---- stage the tiles (rows past N are zero: the reference pads after smoothing)
+  for (int i = tid; i < NV; i += 256) {
+    const int r = i / (D / VEC), c = (i % (D / VEC)) * VEC;
+    uint4 kvv = make_uint4(0, 0, 0, 0), vvv = make_uint4(0, 0, 0, 0);
+    if (r < rows) {
+      kvv = *reinterpret_cast<const uint4*>(row_ptr<T>(kv_in, b, h, n0 + r) + c);
+      vvv = *reinterpret_cast<const uint4*>(row_ptr<T>(v_in, b, h, n0 + r) + c);
+    }
+    *reinterpret_cast<uint4*>(kraw + r * D + c) = kvv;
+    *reinterpret_cast<uint4*>(vraw + r * D + c) = vvv;
+  }
+  if (tid < D) kmu[tid] = means[(static_cast<int64_t>(b) * Ht + Hq + h) * D + tid];
+  __syncthreads();
+
+  // ---- K: smoothed block amax -> scale (quantization.py:151-160)
+  constexpr int PER = 64 * D / 256;  // elements per thread
   double amax = 0.0;
-  for (int r = r0; r < 64; r += ROWS_PER_PASS) {
-    const int n = n0 + r;
-    if (n < n1) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(kv_in, b, h, n) + c8 * VEC);
-      const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        const double x = to_f64<T>(e[i]) - kmu[i];
-        ks[r][c8 * VEC + i] = x;
-        amax = fmax(amax, fabs(x));
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) ks[r][c8 * VEC + i] = 0.0;  // zero padding after smoothing
-    }
+#pragma unroll 8
+  for (int k = 0; k < PER; ++k) {
+    const int e = tid + k * 256, r = e / D, c = e % D;
+    if (r < rows) amax = fmax(amax, fabs(to_f64<T>(kraw[r * D + c]) - kmu[c]));
   }
-  amax = block_max_256(amax, scratch);  // also orders the ks[] writes
+  amax = block_max_256(amax, scratch);
   const double kscale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
+  const double kinv = 1.0 / kscale;
+
+  // ---- K codes: 8 consecutive channels per thread-iteration, one 8-byte store
   int8_t* kdst = k_codes + (static_cast<int64_t>(bh) * Np + n0) * D;
-  for (int r = r0; r < 64; r += ROWS_PER_PASS) {
-    int8_t codes[VEC];
+  for (int g = tid; g < 64 * D / 8; g += 256) {
+    const int r = g / (D / 8), c = (g % (D / 8)) * 8;
+    uint32_t w[2] = {0u, 0u};
+    if (r < rows) {
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) codes[i] = static_cast<int8_t>(quant_int(ks[r][c8 * VEC + i], kscale, qmax));
-    int8_t* o = kdst + static_cast<int64_t>(r) * D + c8 * VEC;
-    if constexpr (VEC == 8) {
-      *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(codes);
-    } else {
-      *reinterpret_cast<uint32_t*>(o) = *reinterpret_cast<const uint32_t*>(codes);
-    }
-  }
-
-  // ---- V: per-channel block max, codes, transpose
-  double vreg[64 / ROWS_PER_PASS][VEC];
-  double cmax[VEC];
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) cmax[i] = 0.0;
-#pragma unroll
-  for (int k = 0; k < 64 / ROWS_PER_PASS; ++k) {
-    const int n = n0 + r0 + k * ROWS_PER_PASS;
-    if (n < n1) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(v_in, b, h, n) + c8 * VEC);
-      const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        vreg[k][i] = to_f64<T>(e[i]);
-        cmax[i] = fmax(cmax[i], fabs(vreg[k][i]));
+      for (int i = 0; i < 8; ++i) {
+        const double x = to_f64<T>(kraw[r * D + c + i]) - kmu[c + i];
+        double q = div_rint(x, kscale, kinv);
+        q = fmin(fmax(q, -static_cast<double>(qmax)), static_cast<double>(qmax));
+        w[i >> 2] |= (static_cast<uint32_t>(static_cast<int>(q)) & 0xFFu) << (8 * (i & 3));
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) vreg[k][i] = 0.0;
     }
-  }
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) vmax_part[r0][c8 * VEC + i] = cmax[i];
-  if (threadIdx.x < D) qmu[threadIdx.x] = 0.0;
-  __syncthreads();
-  float* meta = kv_meta + (static_cast<int64_t>(bh) * n_kb + kb) * (4 + D);
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) {
-    double m = 0.0;
-    for (int r = 0; r < ROWS_PER_PASS; ++r) m = fmax(m, vmax_part[r][c8 * VEC + i]);
-    cmax[i] = m > 0.0 ? m / v_r : 1.0;  // now the channel scale
-  }
-  if (r0 == 0) {
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      meta[4 + c8 * VEC + i] = static_cast<float>(cmax[i]);
-      kv_scale64[(static_cast<int64_t>(bh) * n_kb + kb) * (1 + D) + 1 + c8 * VEC + i] = cmax[i];
-    }
-  }
-  if (threadIdx.x < 4) meta[threadIdx.x] = threadIdx.x == 0 ? static_cast<float>(kscale) : 0.0f;
-  if (threadIdx.x == 0) kv_scale64[(static_cast<int64_t>(bh) * n_kb + kb) * (1 + D)] = kscale;
-#pragma unroll
-  for (int k = 0; k < 64 / ROWS_PER_PASS; ++k) {
-    const int r = r0 + k * ROWS_PER_PASS;
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) vt[c8 * VEC + i][r] = e4m3_from_f64(__ddiv_rn(vreg[k][i], cmax[i]));
-  }
-  __syncthreads();
-  // Each channel row of the transposed tile is 64 contiguous bytes: 4 x 16B per row.
-  uint8_t* vdst = v_codes + static_cast<int64_t>(bh) * D * Np + n0;
-  for (int idx = threadIdx.x; idx < D * 4; idx += 256) {
-    const int c = idx >> 2, part = idx & 3;
-    *reinterpret_cast<uint4*>(vdst + static_cast<int64_t>(c) * Np + part * 16) =
-        *reinterpret_cast<const uint4*>(&vt[c][part * 16]);
+    *reinterpret_cast<uint2*>(kdst + static_cast<int64_t>(r) * D + c) = make_uint2(w[0], w[1]);
   }
 
-  // ---- bias for every query head sharing this KV head: b_j = q_mean . Ks_j (FP64)
+  // ---- V: per-channel block max -> scale (quantization.py:178-188); |x| max is exact in f32
+  float* meta = kv_meta + (static_cast<int64_t>(bh) * n_kb + kb) * (4 + D);
+  double* sc64 = kv_scale64 + (static_cast<int64_t>(bh) * n_kb + kb) * (1 + D);
+  if (tid < D) {
+    float m = 0.0f;
+    for (int r = 0; r < rows; ++r) m = fmaxf(m, fabsf(static_cast<float>(to_f64<T>(vraw[r * D + tid]))));
+    const double sc = m > 0.0f ? static_cast<double>(m) / v_r : 1.0;
+    vsc[tid] = sc;
+    meta[4 + tid] = static_cast<float>(sc);
+    sc64[1 + tid] = sc;
+  }
+  if (tid < 4) meta[tid] = tid == 0 ? static_cast<float>(kscale) : 0.0f;
+  if (tid == 0) sc64[0] = kscale;
+  __syncthreads();
+
+  // ---- V codes, transposed: thread -> (channel, 32-row half); 32 codes -> two 16-byte stores
+  for (int t = tid; t < D * 2; t += 256) {
+    const int c = t >> 1, half = t & 1;
+    const double sc = vsc[c], inv = 1.0 / sc;
+    uint32_t w[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i] = 0u;
+#pragma unroll 8
+    for (int i = 0; i < 32; ++i) {
+      const int r = half * 32 + i;
+      const uint8_t code = e4m3_div(to_f64<T>(vraw[r * D + c]), sc, inv);
+      w[i >> 2] |= static_cast<uint32_t>(code) << (8 * (i & 3));
+    }
+    uint8_t* vdst = v_codes + (static_cast<int64_t>(bh) * D + c) * Np + n0 + half * 32;
+    *reinterpret_cast<uint4*>(vdst) = make_uint4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<uint4*>(vdst + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+  }
+
+  // ---- bias for every query head sharing this KV head: b_j = q_mean . Ks_j (attention.py:288-289)
   const int group = Hq / Hkv;
+  const int r = tid >> 2, qq = tid & 3;  // row, quarter of the channels
   for (int g = 0; g < group; ++g) {
     const int hq = h * group + g;
     __syncthreads();
-    if (threadIdx.x < D)
-      qmu[threadIdx.x] = smoothing ? means[(static_cast<int64_t>(b) * Ht + hq) * D + threadIdx.x] : 0.0;
+    if (tid < D) qmu[tid] = smoothing ? means[(static_cast<int64_t>(b) * Ht + hq) * D + tid] : 0.0;
     __syncthreads();
-    if (threadIdx.x < 64) {
-      const int r = threadIdx.x;
-      double acc = 0.0;
-      for (int c = 0; c < D; ++c) acc = fma(qmu[c], ks[r][c], acc);
+    double acc = 0.0;
+    if (r < rows) {
+#pragma unroll 8
+      for (int c = qq * (D / 4); c < (qq + 1) * (D / 4); ++c)
+        acc = fma(qmu[c], to_f64<T>(kraw[r * D + c]) - kmu[c], acc);
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (qq == 0) {
       const int64_t o = (static_cast<int64_t>(b) * Hq + hq) * Np + n0 + r;
       bias[o] = static_cast<float>(acc);
       bias_l2[o] = static_cast<float>(acc * sm_scale_log2);
@@ -385,10 +397,10 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
   dim3 gk(L.n_kb, L.B * L.Hkv);
   constexpr int kv_smem = kv_smem_bytes<T, D>();
   static bool attr_set = false;  // per template instance; benign race (idempotent)
-  if (!attr_set) {
+  if (!attr_set && kv_smem > 48 * 1024) {
     cudaFuncSetAttribute(quantize_kv_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kv_smem);
-    attr_set = true;
   }
+  attr_set = true;
   quantize_kv_kernel<T, D><<<gk, 256, kv_smem, st>>>(kv, vv, L.Hq, L.Hkv, L.N, L.Np, L.n_kb, L.qmax, L.v_r, L.smoothing,
                                                L.sm_scale_log2, L.means, Ht, L.k_codes, L.v_codes, L.kv_meta,
                                                L.kv_scale64, L.bias, L.bias_l2);

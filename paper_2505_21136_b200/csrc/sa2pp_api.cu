@@ -14,6 +14,7 @@ namespace {
 
 thread_local std::string g_last_error;
 uint32_t* g_debug = nullptr;
+unsigned long long* g_trace = nullptr;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -62,6 +63,11 @@ const char* sa2pp_last_error(void) { return g_last_error.c_str(); }
 
 int sa2pp_set_debug_buffer(void* dbg) {
   g_debug = static_cast<uint32_t*>(dbg);
+  return SA2PP_OK;
+}
+
+int sa2pp_set_trace_buffer(void* buf) {
+  g_trace = static_cast<unsigned long long*>(buf);
   return SA2PP_OK;
 }
 
@@ -227,6 +233,7 @@ int sa2pp_attn_fwd(const sa2pp_problem* p, const sa2pp_quant* qt, const sa2pp_ou
   P.o_sn = out->o_stride[2];
   P.report = report;
   P.debug = g_debug;
+  P.trace = g_trace;
   cudaError_t e = sa2pp::launch_attn(*p, P, *qt, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return SA2PP_OK;

@@ -42,6 +42,7 @@ struct AttnParams {
   int64_t o_sb, o_sh, o_sn;
   sa2pp_report* report;
   uint32_t* debug;
+  unsigned long long* trace;  // optional per-phase clock trace of a few CTAs (development aid)
 };
 
 cudaError_t launch_prepass(const PrepassLaunch& L, cudaStream_t st);
