@@ -30,7 +30,13 @@ from pathlib import Path
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-B_DEFAULT, H_DEFAULT, D_DEFAULT = 4, 32, 128
+# (batch, q heads, kv heads, seq, head_dim, causal) per BASELINE.json config
+WORKLOADS = {
+    "kernel": (4, 32, 32, 16384, 128, False),     # configs[1]: kernel bench, the headline
+    "cogvideox": (2, 30, 30, 17776, 64, False),   # configs[2]
+    "llama": (8, 32, 8, 8192, 128, True),          # configs[3]: GQA 4
+    "longctx": (1, 32, 32, 131072, 128, True),     # configs[4]: Ulysses all-to-all when N > 1
+}
 
 
 def parse():
@@ -39,11 +45,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=B_DEFAULT)
-    ap.add_argument("--heads", type=int, default=H_DEFAULT)
-    ap.add_argument("--seq", type=int, default=16384)
-    ap.add_argument("--head-dim", type=int, default=D_DEFAULT)
-    ap.add_argument("--causal", action="store_true")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="kernel",
+                    help="BASELINE.json configs: kernel (configs[1], the headline), cogvideox, llama, longctx")
+    ap.add_argument("--seq", type=int, default=None, help="override the sequence length")
+    ap.add_argument("--causal", action="store_true", help="causal variant of the kernel workload")
     ap.add_argument("--pv-accum", choices=["fp16", "fp32"], default="fp16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -54,9 +59,25 @@ def ops_of(B, H, N, D, causal):
     return 4.0 * B * H * N * N * D * (0.5 if causal else 1.0)
 
 
+def resolve(a):
+    B, Hq, Hkv, N, D, causal = WORKLOADS[a.workload]
+    if a.seq is not None:
+        N = a.seq
+    if a.causal:
+        causal = True
+    a.batch, a.heads, a.kv_heads, a.seq, a.head_dim, a.causal = B, Hq, Hkv, N, D, causal
+    return a
+
+
 def workload_name(a):
-    return (f"kernel_bench_b{a.batch}_h{a.heads}_n{a.seq}_d{a.head_dim}_"
-            f"{'causal' if a.causal else 'noncausal'}")
+    return (f"{a.workload}_b{a.batch}_h{a.heads}" + (f"kv{a.kv_heads}" if a.kv_heads != a.heads else "")
+            + f"_n{a.seq}_d{a.head_dim}_{'causal' if a.causal else 'noncausal'}")
+
+
+def prepass_bytes(Hq, Hkv, N, D):
+    """Algorithmic HBM bytes of the prepass for bf16 inputs: Q read twice (means, codes), K read
+    twice, V once, int8/e4m3 codes written once; scales/bias are O(N) and ignored."""
+    return N * D * (Hq * (2 * 2 + 1) + Hkv * (2 * 2 + 1 + 2 + 1))
 
 
 def metric_name():
@@ -182,7 +203,7 @@ def run_ours(a):
     import torch
     import torch.distributed as dist
     import paper_2505_21136_b200 as sa
-    from paper_2505_21136_b200 import api, _abi as A
+    from paper_2505_21136_b200 import api, parallel, _abi as A
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -192,29 +213,47 @@ def run_ours(a):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    B, H, N, D = a.batch, a.heads, a.seq, a.head_dim
-    # shard the (batch, head) units across ranks: heads split evenly (no collective on the data path)
-    units = B * H
-    if units % world:
-        raise SystemExit(f"{units} (batch, head) units do not divide over {world} ranks")
-    Bl, Hl = (B, H // world) if H % world == 0 else (B // world, H)
+    B, H, Hkv, N, D = a.batch, a.heads, a.kv_heads, a.seq, a.head_dim
+    group = H // Hkv
+    ulysses = a.workload == "longctx" and world > 1
+    if ulysses:
+        # sequence-sharded input [1, N/P, H, D] per rank; all-to-all to [1, N, H/P, D] and back
+        Ul, Nl = H // world, N // world
+    else:
+        # (batch, head) units sharded across ranks (GQA groups kept whole); no data-path collective
+        Ul, Nl = len(parallel.shard_units(B, H, world, rank, group)), N
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
-    q = torch.randn(Bl, Hl, N, D, device=dev, generator=gen, dtype=torch.float32).bfloat16()
-    k = torch.randn(Bl, Hl, N, D, device=dev, generator=gen, dtype=torch.float32).bfloat16()
-    v = torch.randn(Bl, Hl, N, D, device=dev, generator=gen, dtype=torch.float32).bfloat16()
+    rnd = lambda *shape: torch.randn(*shape, device=dev, generator=gen, dtype=torch.float32).bfloat16()  # noqa: E731
+    if ulysses:
+        xq, xk, xv = rnd(1, Nl, H, D), rnd(1, Nl, H, D), rnd(1, Nl, H, D)
+        q = torch.empty(1, N, Ul, D, device=dev, dtype=torch.bfloat16)  # head-sharded buffers (NHD)
+        k, v = torch.empty_like(q), torch.empty_like(q)
+        layout_strides = lambda t: (t.stride(0), t.stride(2), t.stride(1))  # noqa: E731
+    else:
+        q = rnd(1, Ul, N, D)
+        k, v = rnd(1, Ul // group, N, D), rnd(1, Ul // group, N, D)
+        layout_strides = lambda t: (t.stride(0), t.stride(1), t.stride(2))  # noqa: E731
     out = torch.empty_like(q)
-    prob = api._problem(Bl, Hl, Hl, N, D, causal=a.causal, pv_accum=a.pv_accum)
+    prob = api._problem(1, Ul, Ul // group if not ulysses else Ul, N, D, causal=a.causal, pv_accum=a.pv_accum)
     qt = api.alloc_quant(prob, dev)
     import ctypes
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
     ins = A.Inputs(A.SA2PP_BF16, q.data_ptr(), k.data_ptr(), v.data_ptr(),
-                   (ctypes.c_int64 * 3)(q.stride(0), q.stride(1), q.stride(2)),
-                   (ctypes.c_int64 * 3)(k.stride(0), k.stride(1), k.stride(2)),
-                   (ctypes.c_int64 * 3)(v.stride(0), v.stride(1), v.stride(2)))
-    o = A.Output(A.SA2PP_BF16, out.data_ptr(), (ctypes.c_int64 * 3)(out.stride(0), out.stride(1), out.stride(2)))
+                   (ctypes.c_int64 * 3)(*layout_strides(q)), (ctypes.c_int64 * 3)(*layout_strides(k)),
+                   (ctypes.c_int64 * 3)(*layout_strides(v)))
+    o = A.Output(A.SA2PP_BF16, out.data_ptr(), (ctypes.c_int64 * 3)(*layout_strides(out)))
     qs = qt.struct()
     lib = A.lib()
+
+    def exchange_in():
+        if ulysses:
+            for src, dst in ((xq, q), (xk, k), (xv, v)):
+                dst.copy_(parallel.seq_to_head(src, world))
+
+    def exchange_out():
+        if ulysses:
+            parallel.head_to_seq(out, world)
 
     def prepass():
         A.check(lib.sa2pp_prepass(ctypes.byref(prob), ctypes.byref(ins), ctypes.byref(qs),
@@ -226,8 +265,10 @@ def run_ours(a):
     launches_per_step = 5  # channel_sums, channel_means, quantize_q, quantize_kv, attn_fwd
 
     for _ in range(a.warmup):
+        exchange_in()
         prepass()
         attn()
+        exchange_out()
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
@@ -241,11 +282,13 @@ def run_ours(a):
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for e0, e1, e2 in ev:
+            exchange_in()
             e0.record(stream)
             prepass()
             e1.record(stream)
             attn()
             e2.record(stream)
+            exchange_out()
         t_end.record(stream)
         torch.cuda.synchronize(dev)
         if world > 1:
@@ -258,18 +301,22 @@ def run_ours(a):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, attn_ms, pre_ms = t.tolist()
     ms_per_step = total_ms / a.steps
-    job_ops = ops_of(B, H, N, D, a.causal)
+    job_ops = ops_of(B, H, N, D, a.causal)  # all ranks together
     value = job_ops / (ms_per_step * 1e-3) / 1e12
 
     # ---------------- end-to-end through the public API with pinned host buffers
     e2e = None
     if not a.no_e2e:
-        hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
-        ho = torch.empty(out.shape, dtype=out.dtype, pin_memory=True)
+        src = (xq, xk, xv) if ulysses else (q, k, v)
+        hq, hk, hv = (t.cpu().pin_memory() for t in src)
+        ho = torch.empty(src[0].shape, dtype=out.dtype, pin_memory=True)
 
         def e2e_step():
             dq, dk, dv = (h.to(dev, non_blocking=True) for h in (hq, hk, hv))
-            r = sa.sageattn(dq, dk, dv, "HND", a.causal, None, pv_accum=a.pv_accum, quant=qt, out=out)
+            if ulysses:
+                r = parallel.ulysses_sageattn(dq, dk, dv, a.causal, None, pv_accum=a.pv_accum, quant=qt)
+            else:
+                r = sa.sageattn(dq, dk, dv, "HND", a.causal, None, pv_accum=a.pv_accum, quant=qt, out=out)
             ho.copy_(r, non_blocking=True)
 
         for _ in range(2):
@@ -290,8 +337,8 @@ def run_ours(a):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_ms = t.item()
         e2e = {"value": job_ops / (e2e_ms * 1e-3) / 1e12, "unit": "TOPS",
-               "h2d_bytes_per_step": 3 * q.numel() * q.element_size() * world,
-               "d2h_bytes_per_step": out.numel() * out.element_size() * world,
+               "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in (hq, hk, hv)) * world,
+               "d2h_bytes_per_step": ho.numel() * ho.element_size() * world,
                "ms_per_step": e2e_ms}
 
     if rank != 0:
@@ -301,7 +348,7 @@ def run_ours(a):
 
     bf16_peak, peak_src = read_peaks()
     fp8_peak = 2.0 * bf16_peak  # dense FP8/INT8 tensor rate is 2x dense BF16 on B200
-    attn_ops_per_launch = ops_of(Bl, Hl, N, D, a.causal)
+    attn_ops_per_launch = ops_of(1, Ul, N, D, a.causal)
     achieved = attn_ops_per_launch / (attn_ms * 1e-3) / 1e12
     line = {
         "metric": metric_name(), "value": value, "unit": "TOPS", "n_gpus": world,
@@ -309,16 +356,18 @@ def run_ours(a):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int8 QK / e4m3 PV (fp16 acc)" if a.pv_accum == "fp16" else "int8 QK / e4m3 PV (fp32 acc)",
         "data": "synthetic N(0,1) bf16 Q/K/V",
-        "config": {"workload": workload_name(a), "batch": B, "heads": H, "seq_len": N, "head_dim": D,
-                   "causal": a.causal, "pv_accum": a.pv_accum, "parallelism": f"bh-shard x{world}",
-                   "l2": "inputs larger than L2 (3 x %.0f MB bf16 per GPU)" % (q.numel() * 2 / 1e6)},
+        "config": {"workload": workload_name(a), "batch": B, "heads": H, "kv_heads": Hkv, "seq_len": N,
+                   "head_dim": D, "causal": a.causal, "pv_accum": a.pv_accum,
+                   "parallelism": (f"ulysses x{world}" if ulysses else f"bh-shard x{world}"),
+                   "l2": "inputs larger than L2 (%.0f MB bf16 Q/K/V per GPU)" % (
+                       sum(t.numel() for t in (q, k, v)) * 2 / 1e6)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp8_peak, "traffic": read_traffic(workload_name(a)),
                      "kernel": "attn_fwd_kernel", "ops_per_launch": attn_ops_per_launch,
                      "ms_per_launch": attn_ms, "peak_source": f"2 x bf16 {bf16_peak} ({peak_src})",
                      "frac_of_nominal_4500": achieved / 4500.0},
-        "prepass": {"ms_per_launch": pre_ms, "hbm_bytes": 13 * Bl * Hl * N * D,
-                    "achieved_gbs": 13 * Bl * Hl * N * D / (pre_ms * 1e-3) / 1e9},
+        "prepass": {"ms_per_launch": pre_ms, "hbm_bytes": prepass_bytes(Ul, Ul // group if not ulysses else Ul, N, D),
+                    "achieved_gbs": prepass_bytes(Ul, Ul // group if not ulysses else Ul, N, D) / (pre_ms * 1e-3) / 1e9},
         "gpu_launches": launches_per_step * a.steps,
         "clocks": clk.summary(),
     }
@@ -336,7 +385,7 @@ def run_ours(a):
 
 
 def main():
-    a = parse()
+    a = resolve(parse())
     if a.warmup < 3:
         a.warmup = 3
     if a.impl == "reference":

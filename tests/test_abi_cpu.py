@@ -1,0 +1,123 @@
+"""C-ABI and host-logic checks that need no GPU.
+
+* libsa2pp.so loads and exports every function include/sa2pp.h declares;
+* sa2pp_check_problem / sa2pp_quant_sizes apply the reference's validation rules
+  (attention.py:74-85, 242-245; quantization.py:49-60) with the documented status codes;
+* the Python mirror of AttentionConfig / RangeConfig behaves like the reference's;
+* the product path refuses to run without CUDA (no silent CPU fallback).
+"""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+import torch
+
+import paper_2505_21136_b200 as sa
+from paper_2505_21136_b200 import _abi as A
+from paper_2505_21136_b200.api import _problem
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_functions():
+    text = (ROOT / "include" / "sa2pp.h").read_text()
+    return sorted(set(re.findall(r"SA2PP_API\s+[\w\s\*]+?\b(sa2pp_\w+)\s*\(", text)))
+
+
+def test_header_and_binding_agree():
+    assert declared_functions() == sorted(A.EXPORTED)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = A.lib()
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert lib.sa2pp_version() == 100
+
+
+def rc(**kw):
+    base = dict(B=1, Hq=2, Hkv=2, N=1024, D=64)
+    base.update({k: kw.pop(k) for k in list(kw) if k in base})
+    prob = _problem(base["B"], base["Hq"], base["Hkv"], base["N"], base["D"], causal=False, **kw)
+    return A.lib().sa2pp_check_problem(ctypes.byref(prob))
+
+
+def test_valid_problem():
+    assert rc() == A.SA2PP_OK
+    assert rc(D=128, Hq=32, Hkv=8) == A.SA2PP_OK
+    assert rc(N=1) == A.SA2PP_OK and rc(N=17776) == A.SA2PP_OK
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(D=48), A.SA2PP_ERR_INVALID),            # not a multiple of 32 (attention.py:242-243)
+    (dict(D=96), A.SA2PP_ERR_UNSUPPORTED),        # valid for the reference, not built here
+    (dict(Hq=6, Hkv=4), A.SA2PP_ERR_INVALID),     # GQA group must divide
+    (dict(N=0), A.SA2PP_ERR_INVALID),
+    (dict(qk_bits=6), A.SA2PP_ERR_INVALID),       # attention.py:82-83
+    (dict(p_r=448.0, v_r=448.0), A.SA2PP_ERR_RANGE),          # 2047/depth rule
+    (dict(p_r=448.0, v_r=4.5, depth=2), A.SA2PP_ERR_RANGE),   # 2016 > 1023.5
+    (dict(depth=3), A.SA2PP_ERR_RANGE),
+])
+def test_invalid_problems(kw, code):
+    assert rc(**kw) == code
+    assert A.lib().sa2pp_last_error()
+
+
+def test_range_waiver_and_fp32_baseline_accepted():
+    assert rc(p_r=448.0, v_r=448.0, expect_overflow=True, pv_accum="fp32", depth=1) == A.SA2PP_OK
+
+
+def test_quant_sizes_follow_reference_tiling():
+    prob = _problem(2, 30, 30, 17776, 64, causal=False)
+    sz = A.QuantSizes()
+    assert A.lib().sa2pp_quant_sizes(ctypes.byref(prob), ctypes.byref(sz)) == 0
+    n_qt, n_kb = -(-17776 // 128), -(-17776 // 64)           # 139 query tiles, 278 key blocks
+    assert (n_qt, n_kb) == (139, 278)
+    assert sz.q_codes == 2 * 30 * n_qt * 128 * 64
+    assert sz.k_codes == sz.v_codes == 2 * 30 * n_kb * 64 * 64
+    assert sz.kv_meta == 2 * 30 * n_kb * (4 + 64) * 4
+
+
+def test_config_mirror_matches_reference_rules():
+    for p_r, v_r in sa.TABLE2_PAIRS:
+        assert sa.RangeConfig(p_r, v_r, 2).product == 1008.0
+    with pytest.raises(sa.RangeConfigError):
+        sa.RangeConfig(448.0, 448.0, 1)
+    with pytest.raises(sa.RangeConfigError, match=r"2016 > 1023\.5"):
+        sa.RangeConfig(448.0, 4.5, 2)
+    cfg = sa.AttentionConfig(seq_len=100, head_dim=64)
+    assert cfg.scale == 0.125 and cfg.block_q == 128 and cfg.block_k == 64
+    with pytest.raises(ValueError):
+        sa.AttentionConfig(seq_len=100, head_dim=64, pv_accumulator="fp8")
+
+
+def test_config_mirror_agrees_with_live_reference(lpattn):
+    from lpattn.quantization import RangeConfig as RefRange, RangeConfigError as RefErr
+    for args in [(224.0, 4.5, 2), (448.0, 4.5, 1), (448.0, 448.0, 1), (448.0, 4.5, 2), (112.0, 9.0, 2)]:
+        ok_ref = ok_ours = True
+        try:
+            RefRange(*args)
+        except RefErr:
+            ok_ref = False
+        try:
+            sa.RangeConfig(*args)
+        except sa.RangeConfigError:
+            ok_ours = False
+        assert ok_ref == ok_ours, args
+
+
+def test_no_cpu_fallback():
+    q = torch.zeros(1, 2, 64, 64)
+    with pytest.raises(ValueError, match="CUDA"):
+        sa.sageattn(q, q, q)
+
+
+def test_reference_mirror_rejects_like_reference():
+    import numpy as np
+    z = np.zeros((1, 64, 48))
+    with pytest.raises(ValueError):
+        sa.attention_quantized(z, z, z, sa.AttentionConfig(seq_len=64, head_dim=48))
+    with pytest.raises(ValueError):
+        sa.attention_quantized(z, z, z[:, :32], sa.AttentionConfig(seq_len=64, head_dim=48))

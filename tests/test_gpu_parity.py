@@ -171,3 +171,33 @@ def test_fp32_accumulator_close_to_fp16():
     b = sa.sageattn(q, k, v, pv_accum="fp32").cpu().numpy()
     cos, l1, _ = sa.compare(a, b)
     assert cos >= 0.9999 and l1 <= 1e-3
+
+
+def test_ulysses_single_rank_nccl_equals_direct():
+    """Ulysses path through NCCL (world size 1 on the one-GPU box) equals direct sageattn."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2505_21136_b200.parallel import ulysses_sageattn
+    if not dist.is_initialized():
+        with socket.socket() as s_:
+            s_.bind(("127.0.0.1", 0))
+            port = s_.getsockname()[1]
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    q, k, v = (torch.randn(1, 512, 4, 128, device="cuda", generator=g).bfloat16() for _ in range(3))
+    a = ulysses_sageattn(q, k, v, True)
+    b = sa.sageattn(q, k, v, "NHD", True)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    dist.destroy_process_group()
+
+
+def test_quantize_only_matches_sageattn_prepass():
+    g = load_golden("attn_ragged_causal_d128")
+    q, k, v = (torch.from_numpy(g[x]).cuda()[None] for x in ("q", "k", "v"))
+    qt = sa.quantize(q, k, v)
+    torch.cuda.synchronize()
+    assert np.array_equal(qt.q_codes[0].cpu().numpy()[:, :200], g["q_codes"])
+    assert np.array_equal(qt.k_codes[0].cpu().numpy(), g["k_codes"])
