@@ -75,6 +75,14 @@ __global__ void alu_bench(int iters, float* sink, unsigned long long* cycles) {
       if (OP == 3) u[k] = pack_e4m3x2(a[k], a[k] + 1.f) ^ u[k];  // F2FP e4m3
       if (OP == 4) a[k] = fmax3(a[k], a[(k + 1) & 7] * 0.5f, a[(k + 2) & 7]);  // FMNMX3 (+FMUL)
       if (OP == 5) a[k] = fmaf(a[k], b2, 1e-7f);               // FFMA
+      if (OP == 6) {                                           // HADD2.F32 (f16 -> f32), 2 per reg
+        const __half2 h = *reinterpret_cast<const __half2*>(&u[k]);
+        const float2 g = __half22float2(h);
+        a[k] += g.x * g.y;
+        u[k] += 0x00010001u;
+      }
+      if (OP == 7) a[k] = __int_as_float(static_cast<int>(u[k] += 0x4B400000u)) * b2;  // VIADD magic (+FMUL)
+      if (OP == 8) u[k] = __float_as_uint(__int2float_rn(static_cast<int>(u[k]) >> 3));  // I2F
     }
   }
   const uint64_t t1 = clk();
@@ -169,7 +177,7 @@ int main() {
            warps, warps * 32.0 * 16 * 4 * it / c, warps * 32.0 * 32 * it / c);
   }
   const char* names[] = {"MUFU.EX2(+FMUL)", "FFMA2 (2 flops lanes)", "I2FP(+IADD,FADD)", "F2FP e4m3x2(+LOP)",
-                         "FMNMX3(+FMUL)", "FFMA"};
+                         "FMNMX3(+FMUL)", "FFMA", "HADD2.F32 x2 (+FFMA)", "VIADD magic(+FMUL)", "I2F(+SHF)"};
   for (int warps : {8, 16}) {
     double c;
     c = run(alu_bench<0>, sms, warps * 32, 0, it, sinkf);
@@ -184,6 +192,11 @@ int main() {
     printf("%-24s warps=%2d: %.1f ops/clk/SM\n", names[4], warps, warps * 32.0 * 8 * it / c);
     c = run(alu_bench<5>, sms, warps * 32, 0, it, sinkf);
     printf("%-24s warps=%2d: %.1f ops/clk/SM\n", names[5], warps, warps * 32.0 * 8 * it / c);
+    for (int op = 6; op <= 8; ++op) {
+      c = op == 6 ? run(alu_bench<6>, sms, warps * 32, 0, it, sinkf)
+                  : op == 7 ? run(alu_bench<7>, sms, warps * 32, 0, it, sinkf) : run(alu_bench<8>, sms, warps * 32, 0, it, sinkf);
+      printf("%-24s warps=%2d: %.1f ops/clk/SM\n", names[op], warps, warps * 32.0 * 8 * it / c);
+    }
   }
   const int mit = 20000;
   double c0 = run(umma_bench<0>, sms, 128, 34 * 1024, mit);
