@@ -16,10 +16,17 @@
 // D/2 output accumulators live in registers).  The two resident CTAs run out of phase, so one
 // tile's barrier/MMA waits overlap the other tile's MUFU-bound exp2 phase.
 //
+// Synchronisation per block is split so that no warp waits on the whole CTA before its exp2 work:
+//   * the two warps sharing a row (w, w+4) swap half-row maxima through a 64-thread named barrier;
+//   * the tile-wide P scale (quantization.py:163-175: delta_P = max|P~| / p_r over all 128x64) only
+//     scales P^ *after* exp2: exp2(t - m_row) is computed first, the four h=0 warps publish their
+//     rows' max-shift through a split-phase mbarrier (arrive early, wait after the exponentials),
+//     and P^ = P~ * p_r * 2^-Dt is formed right before the E4M3 pack.
+//
 // Per block each softmax thread: tcgen05.ld S, dequant + bias in the log2 domain, causal/pad mask,
-// half-row max, tile max through one named barrier, online softmax (attention.py:136-154), one
-// E4M3 scale per 128x64 tile (quantization.py:163-175), P^ -> TMEM, promotion of the previous
-// block's PV: O = O*alpha + pv*(dP*dV[c]) (attention.py:303); finally O / l (attention.py:304-305).
+// half-row max, online softmax (attention.py:136-154) with l from the unquantized P~, one E4M3 scale
+// per 128x64 tile, P^ -> TMEM, promotion of the previous block's PV: O = O*alpha + pv*(dP*dV[c])
+// (attention.py:303); finally O / l (attention.py:304-305).
 //
 // TMEM (256 columns per CTA): S[0] cols [0,64), S[1] cols [64,128), PV cols [128, 128+D).  P^ of
 // block j (E4M3, 4 per column) is written over S[j&1]: keys 0-31 at cols [0,8), keys 32-63 at
@@ -37,7 +44,7 @@ namespace sa2pp {
 
 template <int D>
 struct AttnCfg {
-  static constexpr int kStages = (D == 128) ? 5 : 8;
+  static constexpr int kStages = (D == 128) ? 4 : 8;  // powers of two: stage/parity math is masks
   static constexpr int kQBytes = 128 * D;
   static constexpr int kKBytes = 64 * D;
   static constexpr int kVBytes = D * 64;
@@ -55,17 +62,19 @@ struct AttnCfg {
   static constexpr int kOffV = kOffK + kStages * kKBytes;
   static constexpr int kOffMeta = kOffV + kStages * kVBytes;
   static constexpr int kOffBias = kOffMeta + kStages * kMetaBytes;
-  static constexpr int kOffF = kOffBias + kStages * kBiasBytes;     // [2][D]   dP * dV per block parity
-  static constexpr int kOffHalfMax = kOffF + 2 * D * 4;             // [2][2][128] half-row maxima
-  static constexpr int kOffRed = kOffHalfMax + 2 * 2 * 128 * 4;     // [2][8]   warp tile-max candidates
-  static constexpr int kOffL = kOffRed + 2 * 8 * 4;                 // [2][128] final half-row sums
+  static constexpr int kOffF = kOffBias + kStages * kBiasBytes;     // [8][D/2] per-warp dP * dV
+  static constexpr int kOffHalfMax = kOffF + 8 * (D / 2) * 4;             // [2][2][128] half-row maxima
+  static constexpr int kOffRed = kOffHalfMax + 2 * 2 * 128 * 4;     // [2][4]   per-warp max-shift (-Dt candidates)
+  static constexpr int kOffL = kOffRed + 2 * 4 * 4;                 // [2][128] final half-row sums
   static constexpr int kOffCnt = kOffL + 2 * 128 * 4;               // [2] per-parity warp arrival counters
-  static constexpr int kOffBar = kOffCnt + 16;
-  static constexpr int kNumBars = 1 + 2 * kStages + 3;
+  static constexpr int kOffIssue = kOffCnt + 16;                    // IssueState (32 B)
+  static constexpr int kOffBar = kOffIssue + 32;
+  static constexpr int kNumBars = 1 + kStages + 2 + 2 + 1 + 2;
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmemBytes = kOffTmem + 16 + 1024;  // + alignment slack
   static constexpr int kThreads = 256;
   static_assert(2 * kSmemBytes <= 227 * 1024, "two CTAs per SM must fit in shared memory");
+  static_assert((kStages & (kStages - 1)) == 0, "stage count must be a power of two");
 };
 
 template <int N, typename OutT>
@@ -123,23 +132,25 @@ __global__ void __launch_bounds__(256, 2)
   uint64_t* bar_base = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
   uint64_t* q_full = bar_base;
   uint64_t* kv_full = bar_base + 1;
-  uint64_t* kv_empty = bar_base + 1 + S;
-  uint64_t* s_full = bar_base + 1 + 2 * S;  // [2]
+  uint64_t* blk_done = bar_base + 1 + S;   // [2] all eight warps finished block j (P^ stored, PV drained)
+  uint64_t* s_full = blk_done + 2;          // [2]
   uint64_t* pv_full = s_full + 2;           // [1]
-  int* arrive_cnt = reinterpret_cast<int*>(smem + C::kOffCnt);
+  uint64_t* dt_bar = pv_full + 1;           // [2] the four h=0 warps published their max-shift
+  int* issue_cnt = reinterpret_cast<int*>(smem + C::kOffCnt);  // [2] per-parity election counters
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
 
   if (warp == 0) {
     if (lane == 0) {
       mbar_init(q_full, 1);
-      for (int s = 0; s < S; ++s) {
-        mbar_init(&kv_full[s], 1);
-        mbar_init(&kv_empty[s], 1);
-      }
+      for (int s = 0; s < S; ++s) mbar_init(&kv_full[s], 1);
+      mbar_init(&blk_done[0], 8);
+      mbar_init(&blk_done[1], 8);
       mbar_init(&s_full[0], 1);
       mbar_init(&s_full[1], 1);
       mbar_init(pv_full, 1);
-      arrive_cnt[0] = arrive_cnt[1] = 0;
+      mbar_init(&dt_bar[0], 4);
+      mbar_init(&dt_bar[1], 4);
+      issue_cnt[0] = issue_cnt[1] = 0;
       fence_barrier_init();
     }
     __syncwarp();
@@ -150,50 +161,76 @@ __global__ void __launch_bounds__(256, 2)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  // ---------------- MMA / TMA issue helpers (run by one thread at a time)
-  const int kv_row = (b * p.Hkv + hkv) * p.Np;
-  const int vt_row = (b * p.Hkv + hkv) * D;
-  const float* meta_src = p.kv_meta + static_cast<int64_t>(b * p.Hkv + hkv) * p.n_kb * (4 + D);
-  const float* bias_src = p.bias_l2 + static_cast<int64_t>(bh) * p.Np;
+  // ---------------- MMA / TMA issue.  Their per-CTA state lives in shared memory so the softmax
+  // threads do not carry it in registers across the loop.  Issue code runs warp-uniformly in one
+  // elected warp; the single-thread instructions sit under elect.sync.
+  struct IssueState {
+    const float* meta_src;
+    const float* bias_src;
+    int kv_row, vt_row, nblk, tmem;
+  };
+  IssueState* ist = reinterpret_cast<IssueState*>(smem + C::kOffIssue);
+  if (threadIdx.x == 0) {
+    ist->meta_src = p.kv_meta + static_cast<int64_t>(b * p.Hkv + hkv) * p.n_kb * (4 + D);
+    ist->bias_src = p.bias_l2 + static_cast<int64_t>(bh) * p.Np;
+    ist->kv_row = (b * p.Hkv + hkv) * p.Np;
+    ist->vt_row = (b * p.Hkv + hkv) * D;
+    ist->nblk = nblk;
+    ist->tmem = static_cast<int>(tmem);
+  }
   constexpr uint32_t idesc_qk = make_idesc(2u, 1u, 1u, 128u, 64u);             // S32 <- s8 x s8
   constexpr uint32_t idesc_pv = make_idesc(ACC16 ? 0u : 1u, 0u, 0u, 128u, D);  // F16|F32 <- e4m3 x e4m3
-  auto load_block = [&](int j) {
-    const int st = j % S;
+  auto load_block = [&](int j) {  // one thread
+    const int st = static_cast<int>(static_cast<unsigned>(j) % S);
     mbar_arrive_expect_tx(&kv_full[st], C::kKBytes + C::kVBytes + C::kMetaBytes + C::kBiasBytes);
-    tma_load_2d(smem + C::kOffK + st * C::kKBytes, &tm_k, &kv_full[st], 0, kv_row + j * 64);
-    tma_load_2d(smem + C::kOffV + st * C::kVBytes, &tm_v, &kv_full[st], j * 64, vt_row);
-    bulk_load(smem + C::kOffMeta + st * C::kMetaBytes, meta_src + static_cast<int64_t>(j) * (4 + D), C::kMetaBytes,
-              &kv_full[st]);
-    bulk_load(smem + C::kOffBias + st * C::kBiasBytes, bias_src + j * 64, C::kBiasBytes, &kv_full[st]);
+    tma_load_2d(smem + C::kOffK + st * C::kKBytes, &tm_k, &kv_full[st], 0, ist->kv_row + j * 64);
+    tma_load_2d(smem + C::kOffV + st * C::kVBytes, &tm_v, &kv_full[st], j * 64, ist->vt_row);
+    bulk_load(smem + C::kOffMeta + st * C::kMetaBytes, ist->meta_src + static_cast<int64_t>(j) * (4 + D),
+              C::kMetaBytes, &kv_full[st]);
+    bulk_load(smem + C::kOffBias + st * C::kBiasBytes, ist->bias_src + j * 64, C::kBiasBytes, &kv_full[st]);
   };
-  auto issue_qk = [&](int j) {
-    const int st = j % S;
-    mbar_wait(&kv_full[st], (j / S) & 1);
-    tc_fence_after();
+  auto issue_qk = [&](int j, uint32_t tm) {  // one thread; K^_j must have landed
+    const int st = static_cast<int>(static_cast<unsigned>(j) % S);
     const uint64_t qdesc = smem_desc(smem_u32(smem + C::kOffQ), C::kSboQK, C::kLayoutQK);
     const uint64_t kdesc = smem_desc(smem_u32(smem + C::kOffK + st * C::kKBytes), C::kSboQK, C::kLayoutQK);
-    const uint32_t d_tm = tmem + (j & 1) * 64;
+    const uint32_t d_tm = tm + (j & 1) * 64;
 #pragma unroll
     for (int kk = 0; kk < D / 32; ++kk) umma_i8_ss(d_tm, qdesc + 2 * kk, kdesc + 2 * kk, idesc_qk, kk > 0 ? 1u : 0u);
     umma_commit(&s_full[j & 1]);
   };
-  // End of block j, run by the last warp to finish it (every thread has stored P^(j) and drained
-  // PV(j-1)): PV(j), then S(j+2) into the S buffer PV(j) reads (tcgen05 MMAs from one thread
-  // execute in order), then the refill of the stage freed by PV(j-1).
-  auto issue_block_end = [&](int j) {
-    const int st = j % S;
-    const uint64_t vdesc = smem_desc(smem_u32(smem + C::kOffV + st * C::kVBytes), C::kSboV, C::kLayoutV);
-    const uint32_t a_tm = tmem + (j & 1) * 64;
-    umma_f8_ts(tmem + 128, a_tm, vdesc, idesc_pv, 0u);           // keys  0..31: P^ cols [0,8)
-    umma_f8_ts(tmem + 128, a_tm + 32, vdesc + 2, idesc_pv, 1u);  // keys 32..63: P^ cols [32,40)
-    umma_commit(pv_full);
-    umma_commit(&kv_empty[st]);
-    if (j + 2 < nblk) issue_qk(j + 2);  // S[j&1] is free: PV(j), issued above, read P^(j) from it
-    const int jl = j - 1 + S;
-    if (j >= 1 && jl < nblk) {
-      mbar_wait(&kv_empty[(j - 1) % S], ((j - 1) / S) & 1);
-      load_block(jl);
+  // Issued during block j by the first warp to reach its tile-max wait, once every warp has
+  // finished block j-1 (blk_done): PV(j-1) = P^(j-1).V^_{j-1}; S(j+1) into the S buffer PV(j-1)
+  // reads (tcgen05 MMAs from one thread execute in order); the refill of the stage of block j-2,
+  // whose last readers (S(j-2), PV(j-2), promotion of j-2) are all done.  Whole warp, uniform.
+  auto issue_in_block = [&](int j, unsigned long long* tr) {
+    auto istamp = [&](int k) {
+      if constexpr (INSTR) {
+        if (tr != nullptr && j < 64) tr[(2 + j) * 128 + 8 + k] = clock64();
+      }
+    };
+    istamp(0);
+    const int nb = ist->nblk;
+    const uint32_t tm = static_cast<uint32_t>(ist->tmem);
+    mbar_wait_sleep(&blk_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+    tc_fence_after();
+    istamp(1);
+    const int stp = static_cast<int>(static_cast<unsigned>(j - 1) % S);
+    const bool qk = j + 1 < nb;
+    if (qk) mbar_wait(&kv_full[static_cast<unsigned>(j + 1) % S], (static_cast<unsigned>(j + 1) / S) & 1);
+    if (elect_one()) {
+      const uint64_t vdesc = smem_desc(smem_u32(smem + C::kOffV + stp * C::kVBytes), C::kSboV, C::kLayoutV);
+      const uint32_t a_tm = tm + ((j - 1) & 1) * 64;
+      umma_f8_ts(tm + 128, a_tm, vdesc, idesc_pv, 0u);           // keys  0..31: P^ cols [0,8)
+      umma_f8_ts(tm + 128, a_tm + 32, vdesc + 2, idesc_pv, 1u);  // keys 32..63: P^ cols [32,40)
+      umma_commit(pv_full);
+      istamp(2);
+      if (qk) issue_qk(j + 1, tm);
+      istamp(3);
+      const int jl = j - 2 + S;
+      if (j >= 2 && jl < nb) load_block(jl);
+      istamp(4);
     }
+    __syncwarp();
   };
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tm_q);
@@ -203,8 +240,12 @@ __global__ void __launch_bounds__(256, 2)
     tma_load_2d(smem + C::kOffQ, &tm_q, q_full, 0, bh * p.Nq_pad + q0);
     for (int j = 0; j < min(S, nblk); ++j) load_block(j);
     mbar_wait(q_full, 0);
-    issue_qk(0);
-    if (nblk > 1) issue_qk(1);
+    mbar_wait(&kv_full[0], 0);
+    issue_qk(0, tmem);
+    if (nblk > 1) {
+      mbar_wait(&kv_full[1], 0);
+      issue_qk(1, tmem);
+    }
   }
   __syncwarp();
 
@@ -217,16 +258,15 @@ __global__ void __launch_bounds__(256, 2)
   const bool row_valid = row_g < p.N;
   const float a_q = p.q_scale[static_cast<int64_t>(bh) * p.n_qt + qt] * p.sm_scale_log2;
   const uint32_t tm_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
-  float* fbuf = reinterpret_cast<float*>(smem + C::kOffF);
   float* halfmax = reinterpret_cast<float*>(smem + C::kOffHalfMax);
   float* red = reinterpret_cast<float*>(smem + C::kOffRed);
   const bool dbg = INSTR && (p.debug != nullptr) && qt == 0 && bh == 0;
   unsigned long long* trc = (INSTR && p.trace != nullptr && bh == 0 && qt < 8 && lane == 0)
-                                ? p.trace + static_cast<int64_t>(qt) * 66 * 64 + warp * 8
+                                ? p.trace + static_cast<int64_t>(qt) * 66 * 128 + warp * 16
                                 : nullptr;
   auto stamp = [&](int j, int k) {
     if constexpr (INSTR) {
-      if (trc != nullptr && j < 64) trc[(2 + j) * 64 + k] = clock64();
+      if (trc != nullptr && j < 64) trc[(2 + j) * 128 + k] = clock64();
     }
   };
   if constexpr (INSTR) {
@@ -240,16 +280,18 @@ __global__ void __launch_bounds__(256, 2)
   float2 O[HD / 2];
 #pragma unroll
   for (int c = 0; c < HD / 2; ++c) O[c] = make_float2(0.0f, 0.0f);
-  float m_run = -INFINITY, l_half = 0.0f, alpha_prev = 1.0f;
+  float m_run = -INFINITY, l_half = 0.0f, alpha_prev = 1.0f, dp_prev = 1.0f;
   bool resc_prev = true;
   uint32_t overflow = 0;
-  const bool want_overflow = ACC16 && p.report != nullptr;
+  const bool want_overflow = INSTR && ACC16 && p.report != nullptr;
+  // per-warp promotion factors f[c] = dP_j * dV_j[c] for this warp's D/2 channels (written and read
+  // by the same warp, so only __syncwarp orders them)
+  float* fw = reinterpret_cast<float*>(smem + C::kOffF) + warp * HD;
 
   // O[c] = O[c]*alpha + pv[c]*f[c] for this thread's D/2 channels of row r (attention.py:303).
   // RESC: at least one row of the warp changed its running max, so O is rescaled by alpha.
   auto promote_impl = [&](int jj, auto resc_tag) {
     constexpr bool RESC = decltype(resc_tag)::value;
-    const float* f = fbuf + (jj & 1) * D + h * HD;
     const float2 al2 = make_float2(alpha_prev, alpha_prev);
     constexpr int CH = ACC16 ? 32 : 16;  // channels per TMEM load (16 registers either way)
 #pragma unroll
@@ -284,7 +326,7 @@ __global__ void __launch_bounds__(256, 2)
       }
 #pragma unroll
       for (int i = 0; i < CH / 2; i += 2) {
-        const float4 fv = ld_shared_f4(f + c0 + 2 * i);
+        const float4 fv = ld_shared_f4(fw + c0 + 2 * i);
         if constexpr (RESC) {
           O[c0 / 2 + i] = __ffma2_rn(pv[i], make_float2(fv.x, fv.y), __fmul2_rn(O[c0 / 2 + i], al2));
           O[c0 / 2 + i + 1] = __ffma2_rn(pv[i + 1], make_float2(fv.z, fv.w), __fmul2_rn(O[c0 / 2 + i + 1], al2));
@@ -300,9 +342,16 @@ __global__ void __launch_bounds__(256, 2)
       }
     }
   };
+  // Promotion of block jj (its stage's dV is still resident: the stage is refilled two blocks later).
   auto promote = [&](int jj) {
-    mbar_wait(pv_full, jj & 1);
+    {
+      const float* meta = reinterpret_cast<const float*>(smem + C::kOffMeta + (static_cast<unsigned>(jj) % S) * C::kMetaBytes);
+      const float2 dv = *reinterpret_cast<const float2*>(meta + 4 + h * HD + 2 * (lane % (HD / 2)));
+      if (2 * lane < HD) *reinterpret_cast<float2*>(fw + 2 * lane) = make_float2(dp_prev * dv.x, dp_prev * dv.y);
+    }
+    mbar_wait_sleep(pv_full, jj & 1);
     tc_fence_after();
+    __syncwarp();
     stamp(jj + 1, 6);
     if (__any_sync(0xffffffffu, resc_prev)) {
       promote_impl(jj, std::true_type{});
@@ -312,22 +361,23 @@ __global__ void __launch_bounds__(256, 2)
   };
 
   // One key block.  MASK: causal diagonal / padded-tail block (attention.py:128-133, 293-294).
+  // Pass 1 turns S into t (log2-domain scores) in place in TMEM and finds the row max; while the
+  // tile-wide max-shift is gathered the first warp there issues the tensor work; pass 2 reads t
+  // back and forms P^ with the final shift; then the previous block's PV is promoted.
   auto block = [&](int j, auto mask_tag) {
     constexpr bool MASK = decltype(mask_tag)::value;
-    const int st = j % S;
-    mbar_wait(&kv_full[st], (j / S) & 1);
-    mbar_wait(&s_full[j & 1], (j >> 1) & 1);
+    const int st = static_cast<int>(static_cast<unsigned>(j) % S);
+    mbar_wait_sleep(&kv_full[st], (static_cast<unsigned>(j) / S) & 1);
+    mbar_wait_sleep(&s_full[j & 1], (j >> 1) & 1);
     tc_fence_after();
     stamp(j, 0);
     const float* meta = reinterpret_cast<const float*>(smem + C::kOffMeta + st * C::kMetaBytes);
-    const float* cb = reinterpret_cast<const float*>(smem + C::kOffBias + st * C::kBiasBytes) + h * 32;
-    const float a = a_q * ld_shared_f32(meta);
     const uint32_t s_addr = tm_row + (j & 1) * 64 + h * 32;
     // ---- pass 1: t = S_int * (dQ dK sm_scale log2e) + bias_j * sm_scale log2e  (attention.py:287-292)
-    //      and the half-row max; t stays in registers across the tile-max barrier.
-    float2 x[16];
     float hmax;
     {
+      const float* cb = reinterpret_cast<const float*>(smem + C::kOffBias + st * C::kBiasBytes) + h * 32;
+      const float a = a_q * ld_shared_f32(meta);
       uint32_t sr[32];
       tmem_ld32(s_addr, sr);
       tmem_wait_ld();
@@ -339,6 +389,7 @@ __global__ void __launch_bounds__(256, 2)
         }
       }
       const float2 a2 = make_float2(a, a);
+      float2 x[16];
 #pragma unroll
       for (int i = 0; i < 16; i += 2) {
         const float4 c4 = ld_shared_f4(cb + 2 * i);
@@ -362,70 +413,86 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
       for (int i = 1; i < 15; ++i) hmax = fmax3(hmax, x[i].y, x[i + 1].x);
       hmax = fmaxf(hmax, x[15].y);
+      tmem_st32(s_addr, reinterpret_cast<const uint32_t(&)[32]>(x));
     }
-    // Tile-max candidate: rowmax - m_new = min(0, rowmax - m_old) = max over halves of
-    // min(0, halfmax - m_old), so each half contributes without knowing its partner.
-    float d_r = row_valid ? fminf(0.0f, hmax - m_run) : -INFINITY;
-    if (m_run == -INFINITY) d_r = row_valid && hmax != -INFINITY ? 0.0f : d_r;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) d_r = fmaxf(d_r, __shfl_xor_sync(0xffffffffu, d_r, o));
+    // ---- row max: swap half-row maxima with the partner warp (w ^ 4) only
     float* hm_j = halfmax + (j & 1) * 256;
-    float* red_j = red + (j & 1) * 8;
     hm_j[h * 128 + r] = hmax;
-    if (lane == 0) red_j[warp] = d_r;
     stamp(j, 2);
-    named_bar_sync(1, 256);
+    named_bar_sync(1 + wq, 64);
     stamp(j, 3);
     const float rmax = fmaxf(hmax, hm_j[(h ^ 1) * 128 + r]);
-    const float4 ra = ld_shared_f4(red_j), rb = ld_shared_f4(red_j + 4);
-    const float Dt = fmaxf(fmaxf(fmaxf(ra.x, ra.y), fmaxf(ra.z, ra.w)), fmaxf(fmaxf(rb.x, rb.y), fmaxf(rb.z, rb.w)));
     const float m_new = fmaxf(m_run, rmax);
-    const float m_eff = (m_new == -INFINITY) ? 0.0f : (m_new + Dt - p.log2_pr);
-    const float2 nme2 = make_float2(-m_eff, -m_eff);
-    // ---- pass 2: P~/dP = exp2(t - m_new) * p_r / tilemax = exp2(t - m_eff); E4M3 RNE satfinite
-    float2 rs = make_float2(0.0f, 0.0f);
-    uint32_t pk[8];
-    {
-      stamp(j, 4);
-#pragma unroll
-      for (int i = 0; i < 16; i += 2) {
-        const float2 u0 = __fadd2_rn(x[i], nme2);
-        const float2 u1 = __fadd2_rn(x[i + 1], nme2);
-        const float2 e0 = make_float2(ex2(u0.x), ex2(u0.y));
-        const float2 e1 = make_float2(ex2(u1.x), ex2(u1.y));
-        rs = __fadd2_rn(rs, __fadd2_rn(e0, e1));
-        pk[i / 2] = pack_e4m3x2(e0.x, e0.y) | (pack_e4m3x2(e1.x, e1.y) << 16);
+    // ---- tile-max candidate: rowmax - m_new = min(0, rowmax - m_old); the warps of one half
+    //      publish -that (>= 0, +inf for rows that do not count) as float bits, min-reduced.
+    if (h == 0) {
+      const float v = (row_valid && rmax != -INFINITY) ? fmaxf(0.0f, m_run - rmax) : INFINITY;
+      const uint32_t vmin = __reduce_min_sync(0xffffffffu, __float_as_uint(v));
+      if (lane == 0) {
+        red[(j & 1) * 4 + wq] = __uint_as_float(vmin);
+        mbar_arrive(&dt_bar[j & 1]);  // release: the store above is visible to every waiter
       }
+      stamp(j, 13);
     }
-    const float dP = ex2(Dt) * p.inv_pr;  // (tile max of P~) / p_r   (quantization.py:172)
-    const float alpha = ex2(m_run - m_new);
-    l_half = l_half * alpha + (rs.x + rs.y) * dP;
-    if (tid < D) fbuf[(j & 1) * D + tid] = dP * ld_shared_f32(meta + 4 + tid);
-    if (p.report != nullptr && tid == 0) {
+    // ---- one of the h=1 warps (they publish nothing, so they reach this point first) issues
+    //      PV(j-1), S(j+1) and a stage refill while the tile-max candidates are being gathered
+    if (j > 0 && warp == 4 + (j & 3)) issue_in_block(j, trc);
+    const float alpha = (m_new == -INFINITY) ? 1.0f : ex2(m_run - m_new);
+    // ---- pass 2a (before the tile-wide shift is known): e = P~ * p_r = exp2(t - m_new + log2 p_r);
+    //      l accumulates the unquantized P~ (attention.py:149-153)
+    const float m_eff = (m_new == -INFINITY) ? 0.0f : (m_new - p.log2_pr);
+    const float2 nme2 = make_float2(-m_eff, -m_eff);
+    float2 e[16];
+    {
+      tmem_wait_st();  // t stored by pass 1
+      uint32_t tr[32];
+      tmem_ld32(s_addr, tr);
+      tmem_wait_ld();
+      const float2* t2 = reinterpret_cast<const float2*>(tr);
+      float2 rs = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float2 u = __fadd2_rn(t2[i], nme2);
+        e[i] = make_float2(ex2(u.x), ex2(u.y));
+        rs = __fadd2_rn(rs, e[i]);
+      }
+      l_half = l_half * alpha + (rs.x + rs.y) * p.inv_pr;
+    }
+    // ---- tile scale (quantization.py:163-175): dP = max P~ / p_r = 2^Dt / p_r,
+    //      Dt = max over the tile of (rowmax - m_new) <= 0;  P^ = P~ / dP = e * 2^-Dt
+    stamp(j, 14);
+    mbar_wait(&dt_bar[j & 1], (j >> 1) & 1);
+    stamp(j, 4);
+    const float4 rv = ld_shared_f4(red + (j & 1) * 4);
+    float sh = fminf(fminf(rv.x, rv.y), fminf(rv.z, rv.w));  // -Dt >= 0
+    sh = (sh == INFINITY) ? 0.0f : sh;
+    const float dP = ex2(-sh) * p.inv_pr;
+    if (INSTR && p.report != nullptr && tid == 0) {
       atomicMin(&p.report->p_scale_min_bits, __float_as_uint(dP));
       atomicMax(&p.report->p_scale_max_bits, __float_as_uint(dP));
     }
-    // P^(j) goes to TMEM first so its registers are free during the promotion; PV(j) is issued
-    // only once all eight warps have arrived below, which also certifies that PV(j-1) was drained.
+    if (sh != 0.0f) {  // tile-uniform
+      const float sc = ex2(sh);
+      const float2 sc2 = make_float2(sc, sc);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) e[i] = __fmul2_rn(e[i], sc2);
+    }
+    uint32_t pk[8];
+#pragma unroll
+    for (int i = 0; i < 16; i += 2) pk[i / 2] = pack_e4m3x2(e[i].x, e[i].y) | (pack_e4m3x2(e[i + 1].x, e[i + 1].y) << 16);
     stamp(j, 5);
     tmem_st8(s_addr, pk);
-    tmem_wait_st();
+    // ---- promotion of block j-1 (PV(j-1) was issued during this block's tile-max wait)
     if (j > 0) promote(j - 1);
+    tmem_wait_st();
     stamp(j, 7);
+    // P^(j) is in TMEM and PV(j-1) was drained: this warp is done with block j.
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();  // release this warp's P^ stores / PV reads to the last arriver
-      if (atomicAdd(&arrive_cnt[j & 1], 1) == 7) {
-        arrive_cnt[j & 1] = 0;
-        __threadfence_block();
-        tc_fence_after();
-        issue_block_end(j);
-      }
-    }
-    __syncwarp();
+    if (lane == 0) mbar_arrive(&blk_done[j & 1]);
     resc_prev = (m_new != m_run);
     alpha_prev = alpha;
+    dp_prev = dP;
     m_run = m_new;
   };
 
@@ -435,9 +502,24 @@ __global__ void __launch_bounds__(256, 2)
   for (; j < n_plain; ++j) block(j, std::false_type{});
   for (; j < nblk; ++j) block(j, std::true_type{});
 
+  // ---- PV of the last block, then its promotion and the normalisation O / l
+  if (warp == 0) {
+    mbar_wait_sleep(&blk_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
+    tc_fence_after();
+    if (elect_one()) {
+      const uint32_t tm = tmem;
+      const int stp = static_cast<int>(static_cast<unsigned>(nblk - 1) % S);
+      const uint64_t vdesc = smem_desc(smem_u32(smem + C::kOffV + stp * C::kVBytes), C::kSboV, C::kLayoutV);
+      const uint32_t a_tm = tm + ((nblk - 1) & 1) * 64;
+      umma_f8_ts(tm + 128, a_tm, vdesc, idesc_pv, 0u);
+      umma_f8_ts(tm + 128, a_tm + 32, vdesc + 2, idesc_pv, 1u);
+      umma_commit(pv_full);
+    }
+    __syncwarp();
+  }
   float* lbuf = reinterpret_cast<float*>(smem + C::kOffL);
   lbuf[h * 128 + r] = l_half;
-  named_bar_sync(1, 256);  // last block's fbuf and both half-row sums visible
+  named_bar_sync(1 + wq, 64);  // the partner's half-row sum
   promote(nblk - 1);
   if (want_overflow && overflow) atomicAdd(&p.report->overflow_events, overflow);
   if (row_valid) {
@@ -523,11 +605,12 @@ static cudaError_t launch_outi(const AttnParams& P, const sa2pp_quant& qt, cudaS
   }
 }
 
-// Instrumented variants (TMEM dumps, phase traces) are separate instantiations so the production
-// kernel carries no debug branches.
+// Instrumented variants (RunReport counters, TMEM dumps, phase traces) are separate instantiations so
+// the production kernel carries no debug branches.
 template <int D, bool CAUSAL, bool ACC16>
 static cudaError_t launch_out(const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
-  if (P.debug != nullptr || P.trace != nullptr) return launch_outi<D, CAUSAL, ACC16, true>(P, qt, st);
+  if (P.debug != nullptr || P.trace != nullptr || P.report != nullptr)
+    return launch_outi<D, CAUSAL, ACC16, true>(P, qt, st);
   return launch_outi<D, CAUSAL, ACC16, false>(P, qt, st);
 }
 

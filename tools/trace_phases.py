@@ -1,7 +1,9 @@
 """Per-phase clock trace of a few attention CTAs (development aid; needs a GPU).
 
-Stamps per block (thread 0 and thread 128): 0 S ready, 1 S loaded, 2 pass-1 done, 3 after the
-tile-max barrier, 4 t reloaded, 5 exp/pack done, 6 PV(j-1) ready, 7 promotion done.
+Stamps per block and warp (lane 0): 0 S ready, 1 S loaded, 2 pass 1 done, 3 after the pair
+barrier, 4 after the tile-max wait, 5 pass 2 packed, 6 PV(j-1) ready (in the promotion),
+7 block end; issuer-only (lane 0 of the last arriving warp): 8 enter, 9 PV issued,
+10 S(j+2) issued, 11 stage free, 12 refill issued.
 """
 import os
 import sys
@@ -13,27 +15,42 @@ from paper_2505_21136_b200 import _abi as A
 
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
 acc = sys.argv[2] if len(sys.argv) > 2 else "fp16"
-q = torch.randn(4, 32, N, 128, device="cuda", dtype=torch.bfloat16)
+D = int(sys.argv[3]) if len(sys.argv) > 3 else 128
+q = torch.randn(4, 32, N, D, device="cuda", dtype=torch.bfloat16)
 k, v = torch.randn_like(q), torch.randn_like(q)
 sa.sageattn(q, k, v, pv_accum=acc)
-tr = torch.zeros(8 * 66 * 64, dtype=torch.int64, device="cuda")
+tr = torch.zeros(8 * 66 * 128, dtype=torch.int64, device="cuda")
 A.lib().sa2pp_set_trace_buffer(tr.data_ptr())
 sa.sageattn(q, k, v, pv_accum=acc)
 torch.cuda.synchronize()
 A.lib().sa2pp_set_trace_buffer(None)
-t = tr.view(8, 66, 64).cpu().numpy().astype(np.int64)
-names = ["S-wait", "ldS", "pass1", "barrier", "ldT", "exp", "PVwait", "promote", "end->next"]
+t = tr.view(8, 66, 128).cpu().numpy().astype(np.int64)
+names = ["S-ready", "ldS", "pass1", "pairbar", "dt-wait", "pass2", "PV-ready", "end"]
 for cta in range(2):
     smid, g0, g1, nb = t[cta, 0, :4]
-    base = t[cta, 2:2 + min(int(nb), 64), 0].copy()
+    nb = min(int(nb), 64)
+    blk = t[cta, 2:2 + nb, :]
+    base = blk[:, 0]  # warp 0 S-ready
+    print(f"cta{cta} sm{smid} blocks {nb} duration {(g1 - g0) / 1e3:.1f} us")
     for w in range(8):
-        th = 8 * w
-        ph = t[cta, 2:2 + min(int(nb), 64), th:th + 8]
-        arr2 = np.median(ph[2:-1, 2] - base[2:-1])
-        print(f"  warp{w}: pass1-done at +{arr2:.0f} vs warp0 block start, S-ready at +{np.median(ph[2:-1,0]-base[2:-1]):.0f}")
-        nbl = ph.shape[0]
-        d = [np.median(ph[2:nbl - 1, k + 1] - ph[2:nbl - 1, k]) for k in range(7)]
-        nxt = np.median(ph[3:nbl, 0] - ph[2:nbl - 1, 7])
-        blk = np.median(np.diff(ph[2:nbl, 0]))
-        print(f"cta{cta} sm{smid} warp{w} blk {blk:5.0f} | " + " ".join(
-            f"{names[k + 1]} {d[k]:5.0f}" for k in range(7)) + f" | {names[8]} {nxt:5.0f}")
+        ph = blk[:, 16 * w:16 * w + 8]
+        sl = slice(4, nb - 2)
+        rel = [np.median(ph[sl, k] - base[sl]) for k in range(8)]
+        per = np.median(np.diff(ph[2:nb, 0]))
+        x13 = np.median(blk[sl, 16 * w + 13] - base[sl]) if blk[5, 16 * w + 13] else float("nan")
+        x14 = np.median(blk[sl, 16 * w + 14] - base[sl])
+        print(f"  warp{w} block {per:6.0f} | " + " ".join(f"{names[k]} {rel[k]:+6.0f}" for k in range(8))
+              + f" | published {x13:+6.0f} pre-dt-wait {x14:+6.0f}")
+    iss = []
+    for w in range(8):
+        for j in range(4, nb - 2):
+            s_ = blk[j, 16 * w + 8:16 * w + 13]
+            if s_[0] > 0:
+                iss.append((w, s_ - s_[0], s_[0] - base[j]))
+    if iss:
+        ws = [w for w, _, _ in iss]
+        arr = np.array([x for _, x, _ in iss])
+        at = np.array([a for _, _, a in iss])
+        print(f"  issuer warps {np.bincount(ws, minlength=8).tolist()}; enter at {np.median(at):+.0f}; "
+              f"PV issued +{np.median(arr[:, 1]):.0f}, S(j+2) +{np.median(arr[:, 2]):.0f}, "
+              f"stage free +{np.median(arr[:, 3]):.0f}, refill +{np.median(arr[:, 4]):.0f}")
