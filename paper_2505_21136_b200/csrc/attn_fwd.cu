@@ -67,8 +67,7 @@ struct AttnCfg {
   static constexpr int kOffRed = kOffHalfMax + 2 * 2 * 128 * 4;     // [2][4]   per-warp max-shift (-Dt candidates)
   static constexpr int kOffL = kOffRed + 2 * 4 * 4;                 // [2][128] final half-row sums
   static constexpr int kOffCnt = kOffL + 2 * 128 * 4;               // [2] per-parity warp arrival counters
-  static constexpr int kOffIssue = kOffCnt + 16;                    // IssueState (32 B)
-  static constexpr int kOffBar = kOffIssue + 32;
+  static constexpr int kOffBar = kOffCnt + 16;
   static constexpr int kNumBars = 1 + kStages + 2 + 2 + 1 + 2;
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmemBytes = kOffTmem + 16 + 1024;  // + alignment slack
@@ -161,75 +160,69 @@ __global__ void __launch_bounds__(256, 2)
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  // ---------------- MMA / TMA issue.  Their per-CTA state lives in shared memory so the softmax
-  // threads do not carry it in registers across the loop.  Issue code runs warp-uniformly in one
-  // elected warp; the single-thread instructions sit under elect.sync.
-  struct IssueState {
-    const float* meta_src;
-    const float* bias_src;
-    int kv_row, vt_row, nblk, tmem;
-  };
-  IssueState* ist = reinterpret_cast<IssueState*>(smem + C::kOffIssue);
-  if (threadIdx.x == 0) {
-    ist->meta_src = p.kv_meta + static_cast<int64_t>(b * p.Hkv + hkv) * p.n_kb * (4 + D);
-    ist->bias_src = p.bias_l2 + static_cast<int64_t>(bh) * p.Np;
-    ist->kv_row = (b * p.Hkv + hkv) * p.Np;
-    ist->vt_row = (b * p.Hkv + hkv) * D;
-    ist->nblk = nblk;
-    ist->tmem = static_cast<int>(tmem);
-  }
+  // ---------------- MMA / TMA issue.  Runs warp-uniformly in one of the h=1 warps; the single-thread
+  // instructions sit under elect.sync.  Everything here derives from blockIdx and the kernel
+  // parameters only, so it lives in uniform registers, not in the softmax threads' register budget.
+  const int kv_row = (b * p.Hkv + hkv) * p.Np;
+  const int vt_row = (b * p.Hkv + hkv) * D;
+  const float* meta_src = p.kv_meta + static_cast<int64_t>(b * p.Hkv + hkv) * p.n_kb * (4 + D);
+  const float* bias_src = p.bias_l2 + static_cast<int64_t>(bh) * p.Np;
   constexpr uint32_t idesc_qk = make_idesc(2u, 1u, 1u, 128u, 64u);             // S32 <- s8 x s8
   constexpr uint32_t idesc_pv = make_idesc(ACC16 ? 0u : 1u, 0u, 0u, 128u, D);  // F16|F32 <- e4m3 x e4m3
   auto load_block = [&](int j) {  // one thread
     const int st = static_cast<int>(static_cast<unsigned>(j) % S);
     mbar_arrive_expect_tx(&kv_full[st], C::kKBytes + C::kVBytes + C::kMetaBytes + C::kBiasBytes);
-    tma_load_2d(smem + C::kOffK + st * C::kKBytes, &tm_k, &kv_full[st], 0, ist->kv_row + j * 64);
-    tma_load_2d(smem + C::kOffV + st * C::kVBytes, &tm_v, &kv_full[st], j * 64, ist->vt_row);
-    bulk_load(smem + C::kOffMeta + st * C::kMetaBytes, ist->meta_src + static_cast<int64_t>(j) * (4 + D),
-              C::kMetaBytes, &kv_full[st]);
-    bulk_load(smem + C::kOffBias + st * C::kBiasBytes, ist->bias_src + j * 64, C::kBiasBytes, &kv_full[st]);
+    tma_load_2d(smem + C::kOffK + st * C::kKBytes, &tm_k, &kv_full[st], 0, kv_row + j * 64);
+    tma_load_2d(smem + C::kOffV + st * C::kVBytes, &tm_v, &kv_full[st], j * 64, vt_row);
+    bulk_load(smem + C::kOffMeta + st * C::kMetaBytes, meta_src + static_cast<int64_t>(j) * (4 + D), C::kMetaBytes,
+              &kv_full[st]);
+    bulk_load(smem + C::kOffBias + st * C::kBiasBytes, bias_src + j * 64, C::kBiasBytes, &kv_full[st]);
   };
-  auto issue_qk = [&](int j, uint32_t tm) {  // one thread; K^_j must have landed
+  auto issue_qk = [&](int j) {  // one thread; K^_j must have landed
     const int st = static_cast<int>(static_cast<unsigned>(j) % S);
     const uint64_t qdesc = smem_desc(smem_u32(smem + C::kOffQ), C::kSboQK, C::kLayoutQK);
     const uint64_t kdesc = smem_desc(smem_u32(smem + C::kOffK + st * C::kKBytes), C::kSboQK, C::kLayoutQK);
-    const uint32_t d_tm = tm + (j & 1) * 64;
+    const uint32_t d_tm = tmem + (j & 1) * 64;
 #pragma unroll
     for (int kk = 0; kk < D / 32; ++kk) umma_i8_ss(d_tm, qdesc + 2 * kk, kdesc + 2 * kk, idesc_qk, kk > 0 ? 1u : 0u);
     umma_commit(&s_full[j & 1]);
   };
-  // Issued during block j by the first warp to reach its tile-max wait, once every warp has
-  // finished block j-1 (blk_done): PV(j-1) = P^(j-1).V^_{j-1}; S(j+1) into the S buffer PV(j-1)
-  // reads (tcgen05 MMAs from one thread execute in order); the refill of the stage of block j-2,
-  // whose last readers (S(j-2), PV(j-2), promotion of j-2) are all done.  Whole warp, uniform.
-  auto issue_in_block = [&](int j, unsigned long long* tr) {
+  auto issue_pv = [&](int jj) {  // one thread; P^(jj) stored and PV(jj-1) drained by every warp
+    const int stp = static_cast<int>(static_cast<unsigned>(jj) % S);
+    const uint64_t vdesc = smem_desc(smem_u32(smem + C::kOffV + stp * C::kVBytes), C::kSboV, C::kLayoutV);
+    const uint32_t a_tm = tmem + (jj & 1) * 64;
+    umma_f8_ts(tmem + 128, a_tm, vdesc, idesc_pv, 0u);           // keys  0..31: P^ cols [0,8)
+    umma_f8_ts(tmem + 128, a_tm + 32, vdesc + 2, idesc_pv, 1u);  // keys 32..63: P^ cols [32,40)
+    umma_commit(pv_full);
+  };
+  // During block j, once every warp has finished block j-1 (blk_done):
+  //   warp 4 + (j & 3):      PV(j-1) = P^(j-1).V^_{j-1}, then S(j+1) into the S buffer PV(j-1) reads
+  //                          (tcgen05 MMAs from one thread execute in order);
+  //   warp 4 + ((j+2) & 3):  the refill of the stage of block j-2, whose last readers (S(j-2),
+  //                          PV(j-2), the promotion of j-2) are all done.
+  auto issue_mma = [&](int j, unsigned long long* tr) {
     auto istamp = [&](int k) {
       if constexpr (INSTR) {
         if (tr != nullptr && j < 64) tr[(2 + j) * 128 + 8 + k] = clock64();
       }
     };
     istamp(0);
-    const int nb = ist->nblk;
-    const uint32_t tm = static_cast<uint32_t>(ist->tmem);
     mbar_wait_sleep(&blk_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
     tc_fence_after();
     istamp(1);
-    const int stp = static_cast<int>(static_cast<unsigned>(j - 1) % S);
-    const bool qk = j + 1 < nb;
+    const bool qk = j + 1 < nblk;
     if (qk) mbar_wait(&kv_full[static_cast<unsigned>(j + 1) % S], (static_cast<unsigned>(j + 1) / S) & 1);
     if (elect_one()) {
-      const uint64_t vdesc = smem_desc(smem_u32(smem + C::kOffV + stp * C::kVBytes), C::kSboV, C::kLayoutV);
-      const uint32_t a_tm = tm + ((j - 1) & 1) * 64;
-      umma_f8_ts(tm + 128, a_tm, vdesc, idesc_pv, 0u);           // keys  0..31: P^ cols [0,8)
-      umma_f8_ts(tm + 128, a_tm + 32, vdesc + 2, idesc_pv, 1u);  // keys 32..63: P^ cols [32,40)
-      umma_commit(pv_full);
+      issue_pv(j - 1);
       istamp(2);
-      if (qk) issue_qk(j + 1, tm);
+      if (qk) issue_qk(j + 1);
       istamp(3);
-      const int jl = j - 2 + S;
-      if (j >= 2 && jl < nb) load_block(jl);
-      istamp(4);
     }
+    __syncwarp();
+  };
+  auto issue_load = [&](int j) {
+    mbar_wait_sleep(&blk_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+    if (elect_one()) load_block(j - 2 + S);
     __syncwarp();
   };
   if (threadIdx.x == 0) {
@@ -241,10 +234,10 @@ __global__ void __launch_bounds__(256, 2)
     for (int j = 0; j < min(S, nblk); ++j) load_block(j);
     mbar_wait(q_full, 0);
     mbar_wait(&kv_full[0], 0);
-    issue_qk(0, tmem);
+    issue_qk(0);
     if (nblk > 1) {
       mbar_wait(&kv_full[1], 0);
-      issue_qk(1, tmem);
+      issue_qk(1);
     }
   }
   __syncwarp();
@@ -349,7 +342,7 @@ __global__ void __launch_bounds__(256, 2)
       const float2 dv = *reinterpret_cast<const float2*>(meta + 4 + h * HD + 2 * (lane % (HD / 2)));
       if (2 * lane < HD) *reinterpret_cast<float2*>(fw + 2 * lane) = make_float2(dp_prev * dv.x, dp_prev * dv.y);
     }
-    mbar_wait_sleep(pv_full, jj & 1);
+    mbar_wait_sleep(pv_full, static_cast<uint32_t>(jj) & 1u);
     tc_fence_after();
     __syncwarp();
     stamp(jj + 1, 6);
@@ -364,15 +357,16 @@ __global__ void __launch_bounds__(256, 2)
   // Pass 1 turns S into t (log2-domain scores) in place in TMEM and finds the row max; while the
   // tile-wide max-shift is gathered the first warp there issues the tensor work; pass 2 reads t
   // back and forms P^ with the final shift; then the previous block's PV is promoted.
-  auto block = [&](int j, auto mask_tag) {
+  auto block = [&](int j, auto mask_tag, auto par_tag) {
     constexpr bool MASK = decltype(mask_tag)::value;
+    constexpr int P = decltype(par_tag)::value;  // j & 1, a compile-time constant per instantiation
     const int st = static_cast<int>(static_cast<unsigned>(j) % S);
     mbar_wait_sleep(&kv_full[st], (static_cast<unsigned>(j) / S) & 1);
-    mbar_wait_sleep(&s_full[j & 1], (j >> 1) & 1);
+    mbar_wait_sleep(&s_full[P], (j >> 1) & 1);
     tc_fence_after();
     stamp(j, 0);
     const float* meta = reinterpret_cast<const float*>(smem + C::kOffMeta + st * C::kMetaBytes);
-    const uint32_t s_addr = tm_row + (j & 1) * 64 + h * 32;
+    const uint32_t s_addr = tm_row + P * 64 + h * 32;
     // ---- pass 1: t = S_int * (dQ dK sm_scale log2e) + bias_j * sm_scale log2e  (attention.py:287-292)
     float hmax;
     {
@@ -409,14 +403,21 @@ __global__ void __launch_bounds__(256, 2)
           if (key0 + 2 * i + 1 >= lim) x[i].y = -INFINITY;
         }
       }
-      hmax = fmax3(x[0].x, x[0].y, x[1].x);
+      {  // four independent max chains (latency), then combine
+        float m4[4];
 #pragma unroll
-      for (int i = 1; i < 15; ++i) hmax = fmax3(hmax, x[i].y, x[i + 1].x);
-      hmax = fmaxf(hmax, x[15].y);
+        for (int q4 = 0; q4 < 4; ++q4) {
+          m4[q4] = fmax3(x[4 * q4].x, x[4 * q4].y, x[4 * q4 + 1].x);
+          m4[q4] = fmax3(m4[q4], x[4 * q4 + 1].y, x[4 * q4 + 2].x);
+          m4[q4] = fmax3(m4[q4], x[4 * q4 + 2].y, x[4 * q4 + 3].x);
+          m4[q4] = fmaxf(m4[q4], x[4 * q4 + 3].y);
+        }
+        hmax = fmaxf(fmax3(m4[0], m4[1], m4[2]), m4[3]);
+      }
       tmem_st32(s_addr, reinterpret_cast<const uint32_t(&)[32]>(x));
     }
     // ---- row max: swap half-row maxima with the partner warp (w ^ 4) only
-    float* hm_j = halfmax + (j & 1) * 256;
+    float* hm_j = halfmax + P * 256;
     hm_j[h * 128 + r] = hmax;
     stamp(j, 2);
     named_bar_sync(1 + wq, 64);
@@ -429,14 +430,15 @@ __global__ void __launch_bounds__(256, 2)
       const float v = (row_valid && rmax != -INFINITY) ? fmaxf(0.0f, m_run - rmax) : INFINITY;
       const uint32_t vmin = __reduce_min_sync(0xffffffffu, __float_as_uint(v));
       if (lane == 0) {
-        red[(j & 1) * 4 + wq] = __uint_as_float(vmin);
-        mbar_arrive(&dt_bar[j & 1]);  // release: the store above is visible to every waiter
+        red[P * 4 + wq] = __uint_as_float(vmin);
+        mbar_arrive(&dt_bar[P]);  // release: the store above is visible to every waiter
       }
       stamp(j, 13);
     }
     // ---- one of the h=1 warps (they publish nothing, so they reach this point first) issues
     //      PV(j-1), S(j+1) and a stage refill while the tile-max candidates are being gathered
-    if (j > 0 && warp == 4 + (j & 3)) issue_in_block(j, trc);
+    if (j > 0 && warp == 4 + (j & 3)) issue_mma(j, trc);
+    if (j >= 2 && j - 2 + S < nblk && warp == 4 + ((j + 2) & 3)) issue_load(j);
     const float alpha = (m_new == -INFINITY) ? 1.0f : ex2(m_run - m_new);
     // ---- pass 2a (before the tile-wide shift is known): e = P~ * p_r = exp2(t - m_new + log2 p_r);
     //      l accumulates the unquantized P~ (attention.py:149-153)
@@ -449,21 +451,23 @@ __global__ void __launch_bounds__(256, 2)
       tmem_ld32(s_addr, tr);
       tmem_wait_ld();
       const float2* t2 = reinterpret_cast<const float2*>(tr);
-      float2 rs = make_float2(0.0f, 0.0f);
+      float2 rs[4] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f),
+                      make_float2(0.0f, 0.0f)};
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const float2 u = __fadd2_rn(t2[i], nme2);
         e[i] = make_float2(ex2(u.x), ex2(u.y));
-        rs = __fadd2_rn(rs, e[i]);
+        rs[i & 3] = __fadd2_rn(rs[i & 3], e[i]);
       }
-      l_half = l_half * alpha + (rs.x + rs.y) * p.inv_pr;
+      const float2 r2 = __fadd2_rn(__fadd2_rn(rs[0], rs[1]), __fadd2_rn(rs[2], rs[3]));
+      l_half = l_half * alpha + (r2.x + r2.y) * p.inv_pr;
     }
     // ---- tile scale (quantization.py:163-175): dP = max P~ / p_r = 2^Dt / p_r,
     //      Dt = max over the tile of (rowmax - m_new) <= 0;  P^ = P~ / dP = e * 2^-Dt
     stamp(j, 14);
-    mbar_wait(&dt_bar[j & 1], (j >> 1) & 1);
+    mbar_wait(&dt_bar[P], (j >> 1) & 1);
     stamp(j, 4);
-    const float4 rv = ld_shared_f4(red + (j & 1) * 4);
+    const float4 rv = ld_shared_f4(red + P * 4);
     float sh = fminf(fminf(rv.x, rv.y), fminf(rv.z, rv.w));  // -Dt >= 0
     sh = (sh == INFINITY) ? 0.0f : sh;
     const float dP = ex2(-sh) * p.inv_pr;
@@ -489,7 +493,7 @@ __global__ void __launch_bounds__(256, 2)
     // P^(j) is in TMEM and PV(j-1) was drained: this warp is done with block j.
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&blk_done[j & 1]);
+    if (lane == 0) mbar_arrive(&blk_done[P]);
     resc_prev = (m_new != m_run);
     alpha_prev = alpha;
     dp_prev = dP;
@@ -499,22 +503,29 @@ __global__ void __launch_bounds__(256, 2)
   // Blocks entirely below the causal diagonal and inside the sequence need no mask.
   const int n_plain = CAUSAL ? min(nblk, q0 / 64) : ((p.N % 64 == 0) ? nblk : nblk - 1);
   int j = 0;
-  for (; j < n_plain; ++j) block(j, std::false_type{});
-  for (; j < nblk; ++j) block(j, std::true_type{});
+  using P0 = std::integral_constant<int, 0>;
+  using P1 = std::integral_constant<int, 1>;
+  for (; j + 1 < n_plain; j += 2) {
+    block(j, std::false_type{}, P0{});
+    block(j + 1, std::false_type{}, P1{});
+  }
+  if (j < n_plain) {
+    block(j, std::false_type{}, P0{});
+    ++j;
+  }
+  for (; j < nblk; ++j) {
+    if (j & 1) {
+      block(j, std::true_type{}, P1{});
+    } else {
+      block(j, std::true_type{}, P0{});
+    }
+  }
 
   // ---- PV of the last block, then its promotion and the normalisation O / l
   if (warp == 0) {
     mbar_wait_sleep(&blk_done[(nblk - 1) & 1], ((nblk - 1) >> 1) & 1);
     tc_fence_after();
-    if (elect_one()) {
-      const uint32_t tm = tmem;
-      const int stp = static_cast<int>(static_cast<unsigned>(nblk - 1) % S);
-      const uint64_t vdesc = smem_desc(smem_u32(smem + C::kOffV + stp * C::kVBytes), C::kSboV, C::kLayoutV);
-      const uint32_t a_tm = tm + ((nblk - 1) & 1) * 64;
-      umma_f8_ts(tm + 128, a_tm, vdesc, idesc_pv, 0u);
-      umma_f8_ts(tm + 128, a_tm + 32, vdesc + 2, idesc_pv, 1u);
-      umma_commit(pv_full);
-    }
+    if (elect_one()) issue_pv(nblk - 1);
     __syncwarp();
   }
   float* lbuf = reinterpret_cast<float*>(smem + C::kOffL);

@@ -2,8 +2,8 @@
 
 Stamps per block and warp (lane 0): 0 S ready, 1 S loaded, 2 pass 1 done, 3 after the pair
 barrier, 4 after the tile-max wait, 5 pass 2 packed, 6 PV(j-1) ready (in the promotion),
-7 block end; issuer-only (lane 0 of the last arriving warp): 8 enter, 9 PV issued,
-10 S(j+2) issued, 11 stage free, 12 refill issued.
+7 block end; MMA issuer only: 8 enter, 9 blk_done(j-1) seen,
+10 PV(j-1) issued, 11 S(j+1) issued; 13 published (h=0), 14 before the tile-max wait.
 """
 import os
 import sys
@@ -44,13 +44,13 @@ for cta in range(2):
     iss = []
     for w in range(8):
         for j in range(4, nb - 2):
-            s_ = blk[j, 16 * w + 8:16 * w + 13]
+            s_ = blk[j, 16 * w + 8:16 * w + 12]
             if s_[0] > 0:
                 iss.append((w, s_ - s_[0], s_[0] - base[j]))
     if iss:
         ws = [w for w, _, _ in iss]
         arr = np.array([x for _, x, _ in iss])
         at = np.array([a for _, _, a in iss])
-        print(f"  issuer warps {np.bincount(ws, minlength=8).tolist()}; enter at {np.median(at):+.0f}; "
-              f"PV issued +{np.median(arr[:, 1]):.0f}, S(j+2) +{np.median(arr[:, 2]):.0f}, "
-              f"stage free +{np.median(arr[:, 3]):.0f}, refill +{np.median(arr[:, 4]):.0f}")
+        print(f"  MMA issuer warps {np.bincount(ws, minlength=8).tolist()}; enter at {np.median(at):+.0f}; "
+              f"blk_done +{np.median(arr[:, 1]):.0f}, PV(j-1) issued +{np.median(arr[:, 2]):.0f}, "
+              f"S(j+1) issued +{np.median(arr[:, 3]):.0f}")
