@@ -46,6 +46,15 @@ __device__ __forceinline__ void dd_add(double& hi, double& lo, double x) {
   hi = s;
 }
 
+template <typename T>
+__device__ __forceinline__ float to_f32(T x);
+template <>
+__device__ __forceinline__ float to_f32<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ float to_f32<__half>(__half x) { return __half2float(x); }
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 x) { return __bfloat162float(x); }
+
 // Input element (b, h, n, c) with strides in elements; channel dim contiguous.
 struct InView {
   const void* base;
@@ -135,13 +144,6 @@ __device__ __forceinline__ double block_max_256(double x, double* scratch) {
   return m;
 }
 
-// RNE of x/scale, clipped to +-qmax: the reference's np.clip(np.round(x / scale)).
-__device__ __forceinline__ int quant_int(double x, double scale, int qmax) {
-  double q = rint(__ddiv_rn(x, scale));
-  q = fmin(fmax(q, -static_cast<double>(qmax)), static_cast<double>(qmax));
-  return static_cast<int>(q);
-}
-
 // Direct FP64 -> E4M3 ("fn") with RNE and saturation to +-448 (numerics.py:152-182).
 __device__ __forceinline__ uint8_t e4m3_from_f64(double x) {
   const uint8_t sign = signbit(x) ? 0x80 : 0x00;
@@ -160,61 +162,6 @@ __device__ __forceinline__ uint8_t e4m3_from_f64(double x) {
   return sign | static_cast<uint8_t>(((e + 7) << 3) | (static_cast<int>(q) - 8));
 }
 
-// ------------------------------------------------------------------ pass 2: Q tiles
-// One CTA (256 threads) per 128-row tile of one (b, hq).  Rows >= N are written as zero codes.
-template <typename T, int D>
-__global__ void __launch_bounds__(256) quantize_q_kernel(InView qv, int Hq, int N, int Nq_pad, int n_qt, int qmax,
-                                                         const double* __restrict__ means, int Ht,
-                                                         int8_t* __restrict__ q_codes, float* __restrict__ q_scale,
-                                                         double* __restrict__ q_scale64) {
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int LANES_PER_ROW = D / VEC;
-  constexpr int ROWS_PER_PASS = 256 / LANES_PER_ROW;
-  __shared__ double scratch[8];
-  const int qt = blockIdx.x;
-  const int bh = blockIdx.y;
-  const int b = bh / Hq, h = bh % Hq;
-  const int c8 = threadIdx.x % LANES_PER_ROW;
-  const int r0 = threadIdx.x / LANES_PER_ROW;
-  const int n0 = qt * 128;
-  const int n1 = min(N, n0 + 128);
-  double mu[VEC];
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) mu[i] = means[(static_cast<int64_t>(b) * Ht + h) * D + c8 * VEC + i];
-  double amax = 0.0;
-  for (int n = n0 + r0; n < n1; n += ROWS_PER_PASS) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(qv, b, h, n) + c8 * VEC);
-    const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) amax = fmax(amax, fabs(to_f64<T>(e[i]) - mu[i]));
-  }
-  amax = block_max_256(amax, scratch);
-  const double scale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
-  if (threadIdx.x == 0) {
-    q_scale[static_cast<int64_t>(bh) * n_qt + qt] = static_cast<float>(scale);
-    q_scale64[static_cast<int64_t>(bh) * n_qt + qt] = scale;
-  }
-  int8_t* dst = q_codes + (static_cast<int64_t>(bh) * Nq_pad) * D;
-  for (int n = n0 + r0; n < n0 + 128; n += ROWS_PER_PASS) {
-    int8_t codes[VEC];
-    if (n < n1) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(qv, b, h, n) + c8 * VEC);
-      const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) codes[i] = static_cast<int8_t>(quant_int(to_f64<T>(e[i]) - mu[i], scale, qmax));
-    } else {
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) codes[i] = 0;
-    }
-    int8_t* o = dst + static_cast<int64_t>(n) * D + c8 * VEC;
-    if constexpr (VEC == 8) {
-      *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(codes);
-    } else {
-      *reinterpret_cast<uint32_t*>(o) = *reinterpret_cast<const uint32_t*>(codes);
-    }
-  }
-}
-
 // x / scale rounded to nearest-even, bit-identical to the FP64 division the reference does
 // (np.round(x / scale)): multiply by the reciprocal and fall back to the correctly rounded
 // division only when the product lies within 1e-9 of a rounding tie.
@@ -223,6 +170,23 @@ __device__ __forceinline__ double div_rint(double x, double scale, double inv) {
   const double fr = fabs(q - trunc(q));
   if (fabs(fr - 0.5) < 1e-9) q = __ddiv_rn(x, scale);
   return rint(q);
+}
+
+
+// INT8/INT4 code of (v - mu) / scale (FP64 in the reference, quantization.py:151-160), fast path.
+// x32 = (v - mu_hi) - mu_lo and q = x32 * fl32(1/scale) in FP32 stay within 4e-5 of the exact
+// quotient whenever |mu| <= 2^16 * amax (the caller checks this per tile), so unless q is within 1e-4
+// of a rounding tie its RNE (magic-number add, exact for |q| < 2^22) is the reference's code; near a
+// tie the FP64 path decides.  No FP64 or conversion (XU) instruction on the common path.
+__device__ __forceinline__ int int_code_fast(float v, float mu_hi, float mu_lo, double mu, float inv32,
+                                             double scale, double inv64, int qmax) {
+  const float x = (v - mu_hi) - mu_lo;
+  const float q = x * inv32;
+  const float t = q + 12582912.0f;  // 1.5 * 2^23
+  const float r = t - 12582912.0f;
+  int c = __float_as_int(t) - 0x4B400000;
+  if (fabsf(fabsf(q - r) - 0.5f) < 1e-4f) c = static_cast<int>(div_rint(static_cast<double>(v) - mu, scale, inv64));
+  return min(max(c, -qmax), qmax);
 }
 
 // E4M3 code of x / scale, bit-identical to encoding the correctly rounded FP64 quotient: the
@@ -240,6 +204,118 @@ __device__ __forceinline__ uint8_t e4m3_div(double x, double scale, double inv) 
   return e4m3_from_f64(q);
 }
 
+
+// E4M3 code of v / scale for the V quantizer, fast path.  q = v * fl32(1/scale) in FP32 is within
+// 2 f32 ulps of the exact quotient (two roundings of 2^-24), so unless q sits within 64 ulps of an
+// E4M3 rounding tie the hardware RNE-satfinite conversion of q gives the same code as encoding the
+// correctly rounded FP64 quotient (numerics.py:152-182); near a tie the exact FP64 path decides.
+__device__ __forceinline__ uint8_t e4m3_div_fast(float v, double scale, double inv64, float inv32) {
+  const float q = v * inv32;
+  const uint32_t a = __float_as_uint(q) & 0x7FFFFFFFu;
+  bool near_tie;
+  if (a >= 0x3C800000u) {  // |q| >= 2^-6: normal E4M3, 20 discarded mantissa bits
+    const uint32_t d = a & 0xFFFFFu;
+    near_tie = d > 0x80000u - 64u && d < 0x80000u + 64u;
+  } else {  // subnormal E4M3: step 2^-9, ties at odd multiples of 2^-10 (q * 512 is exact)
+    const float y = __uint_as_float(a) * 512.0f;
+    near_tie = fabsf((y - truncf(y)) - 0.5f) < 1e-4f;
+  }
+  if (near_tie) return e4m3_div(static_cast<double>(v), scale, inv64);
+  uint16_t r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(0.0f), "f"(q));
+  return static_cast<uint8_t>(r & 0xFF);
+}
+
+// ------------------------------------------------------------------ pass 2: Q tiles
+// One CTA (256 threads) per 128-row tile of one (b, hq).  Rows >= N are written as zero codes.
+// amax = max over channels of max(|max_c - mu_c|, |min_c - mu_c|): fl64(v - mu) is monotone in v, so
+// this is the reference's max |fl64(v - mu)| over the tile with FP64 work per channel only.
+template <typename T, int D>
+__global__ void __launch_bounds__(256) quantize_q_kernel(InView qv, int Hq, int N, int Nq_pad, int n_qt, int qmax,
+                                                         const double* __restrict__ means, int Ht,
+                                                         int8_t* __restrict__ q_codes, float* __restrict__ q_scale,
+                                                         double* __restrict__ q_scale64) {
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int LANES_PER_ROW = D / VEC;
+  constexpr int ROWS_PER_PASS = 256 / LANES_PER_ROW;
+  __shared__ double scratch[8];
+  const int qt = blockIdx.x;
+  const int bh = blockIdx.y;
+  const int b = bh / Hq, h = bh % Hq;
+  const int c8 = threadIdx.x % LANES_PER_ROW;
+  const int r0 = threadIdx.x / LANES_PER_ROW;
+  const int n0 = qt * 128;
+  const int n1 = min(N, n0 + 128);
+  float mn[VEC], mx[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    mn[i] = INFINITY;
+    mx[i] = -INFINITY;
+  }
+  for (int n = n0 + r0; n < n1; n += ROWS_PER_PASS) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(qv, b, h, n) + c8 * VEC);
+    const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      const float x = to_f32<T>(e[i]);
+      mn[i] = fminf(mn[i], x);
+      mx[i] = fmaxf(mx[i], x);
+    }
+  }
+  const double* mup = means + (static_cast<int64_t>(b) * Ht + h) * D + c8 * VEC;
+  double amax = 0.0, mumax = 0.0;
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const double m = mup[i];
+    if (mx[i] >= mn[i])
+      amax = fmax(amax, fmax(fabs(static_cast<double>(mx[i]) - m), fabs(static_cast<double>(mn[i]) - m)));
+    mumax = fmax(mumax, fabs(m));
+  }
+  amax = block_max_256(amax, scratch);
+  mumax = block_max_256(mumax, scratch);
+  const double scale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
+  if (threadIdx.x == 0) {
+    q_scale[static_cast<int64_t>(bh) * n_qt + qt] = static_cast<float>(scale);
+    q_scale64[static_cast<int64_t>(bh) * n_qt + qt] = scale;
+  }
+  const double inv = 1.0 / scale;
+  const float inv32 = static_cast<float>(inv);
+  const bool fast = mumax <= 65536.0 * amax;  // the error bound of int_code_fast
+  float mu_hi[VEC], mu_lo[VEC];
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    mu_hi[i] = static_cast<float>(mup[i]);
+    mu_lo[i] = static_cast<float>(mup[i] - static_cast<double>(mu_hi[i]));
+  }
+  int8_t* dst = q_codes + (static_cast<int64_t>(bh) * Nq_pad) * D;
+  for (int n = n0 + r0; n < n0 + 128; n += ROWS_PER_PASS) {
+    uint32_t w[VEC / 4];
+#pragma unroll
+    for (int i = 0; i < VEC / 4; ++i) w[i] = 0u;
+    if (n < n1) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(qv, b, h, n) + c8 * VEC);
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        const float v = to_f32<T>(e[i]);
+        int c;
+        if (fast) {
+          c = int_code_fast(v, mu_hi[i], mu_lo[i], mup[i], inv32, scale, inv, qmax);
+        } else {
+          c = min(max(static_cast<int>(div_rint(static_cast<double>(v) - mup[i], scale, inv)), -qmax), qmax);
+        }
+        w[i >> 2] |= (static_cast<uint32_t>(c) & 0xFFu) << (8 * (i & 3));
+      }
+    }
+    int8_t* o = dst + static_cast<int64_t>(n) * D + c8 * VEC;
+    if constexpr (VEC == 8) {
+      *reinterpret_cast<uint2*>(o) = make_uint2(w[0], w[1]);
+    } else {
+      *reinterpret_cast<uint32_t*>(o) = w[0];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ pass 3: K/V blocks
 // One CTA (256 threads) per 64-key block of one (b, hkv).  The raw K and V tiles are staged in
 // shared memory once; everything else works from there.
@@ -249,7 +325,7 @@ __device__ __forceinline__ uint8_t e4m3_div(double x, double scale, double inv) 
 //   bias     [B, Hq, Np]              f32 q_mean . Ks_j ; bias_l2 = bias * sm_scale * log2(e)
 template <typename T, int D>
 __host__ __device__ constexpr int kv_smem_bytes() {
-  return 2 * 64 * D * static_cast<int>(sizeof(T)) + 3 * D * 8 + 64;
+  return 2 * 64 * D * static_cast<int>(sizeof(T)) + 3 * D * 8 + 2 * D * 4 + 64;
 }
 
 template <typename T, int D>
@@ -268,6 +344,8 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v
   double* kmu = reinterpret_cast<double*>(kv_smem + 2 * 64 * D * sizeof(T));
   double* qmu = kmu + D;
   double* vsc = qmu + D;
+  float* kmu_hi = reinterpret_cast<float*>(vsc + D);
+  float* kmu_lo = kmu_hi + D;
   __shared__ double scratch[8];
   const int kb = blockIdx.x;
   const int bh = blockIdx.y;
@@ -287,20 +365,35 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v
     *reinterpret_cast<uint4*>(kraw + r * D + c) = kvv;
     *reinterpret_cast<uint4*>(vraw + r * D + c) = vvv;
   }
-  if (tid < D) kmu[tid] = means[(static_cast<int64_t>(b) * Ht + Hq + h) * D + tid];
+  if (tid < D) {
+    const double m = means[(static_cast<int64_t>(b) * Ht + Hq + h) * D + tid];
+    kmu[tid] = m;
+    kmu_hi[tid] = static_cast<float>(m);
+    kmu_lo[tid] = static_cast<float>(m - static_cast<double>(kmu_hi[tid]));
+  }
   __syncthreads();
 
-  // ---- K: smoothed block amax -> scale (quantization.py:151-160)
-  constexpr int PER = 64 * D / 256;  // elements per thread
-  double amax = 0.0;
-#pragma unroll 8
-  for (int k = 0; k < PER; ++k) {
-    const int e = tid + k * 256, r = e / D, c = e % D;
-    if (r < rows) amax = fmax(amax, fabs(to_f64<T>(kraw[r * D + c]) - kmu[c]));
+  // ---- K: smoothed block amax -> scale (quantization.py:151-160) from per-channel min/max
+  //      (fl64(k - mu) is monotone in k: same value as the element-wise FP64 max)
+  double amax = 0.0, mumax = 0.0;
+  {
+    constexpr int TPC = 256 / D;  // threads per channel
+    const int c = tid % D;
+    float mn = INFINITY, mx = -INFINITY;
+    for (int r = tid / D; r < rows; r += TPC) {
+      const float x = to_f32<T>(kraw[r * D + c]);
+      mn = fminf(mn, x);
+      mx = fmaxf(mx, x);
+    }
+    if (mx >= mn) amax = fmax(fabs(static_cast<double>(mx) - kmu[c]), fabs(static_cast<double>(mn) - kmu[c]));
+    mumax = fabs(kmu[c]);
   }
   amax = block_max_256(amax, scratch);
+  mumax = block_max_256(mumax, scratch);
   const double kscale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
   const double kinv = 1.0 / kscale;
+  const float kinv32 = static_cast<float>(kinv);
+  const bool kfast = mumax <= 65536.0 * amax;  // the error bound of int_code_fast
 
   // ---- K codes: 8 consecutive channels per thread-iteration, one 8-byte store
   int8_t* kdst = k_codes + (static_cast<int64_t>(bh) * Np + n0) * D;
@@ -310,10 +403,14 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v
     if (r < rows) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const double x = to_f64<T>(kraw[r * D + c + i]) - kmu[c + i];
-        double q = div_rint(x, kscale, kinv);
-        q = fmin(fmax(q, -static_cast<double>(qmax)), static_cast<double>(qmax));
-        w[i >> 2] |= (static_cast<uint32_t>(static_cast<int>(q)) & 0xFFu) << (8 * (i & 3));
+        const float v = to_f32<T>(kraw[r * D + c + i]);
+        int q;
+        if (kfast) {
+          q = int_code_fast(v, kmu_hi[c + i], kmu_lo[c + i], kmu[c + i], kinv32, kscale, kinv, qmax);
+        } else {
+          q = min(max(static_cast<int>(div_rint(static_cast<double>(v) - kmu[c + i], kscale, kinv)), -qmax), qmax);
+        }
+        w[i >> 2] |= (static_cast<uint32_t>(q) & 0xFFu) << (8 * (i & 3));
       }
     }
     *reinterpret_cast<uint2*>(kdst + static_cast<int64_t>(r) * D + c) = make_uint2(w[0], w[1]);
@@ -324,7 +421,7 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v
   double* sc64 = kv_scale64 + (static_cast<int64_t>(bh) * n_kb + kb) * (1 + D);
   if (tid < D) {
     float m = 0.0f;
-    for (int r = 0; r < rows; ++r) m = fmaxf(m, fabsf(static_cast<float>(to_f64<T>(vraw[r * D + tid]))));
+    for (int r = 0; r < rows; ++r) m = fmaxf(m, fabsf(to_f32<T>(vraw[r * D + tid])));
     const double sc = m > 0.0f ? static_cast<double>(m) / v_r : 1.0;
     vsc[tid] = sc;
     meta[4 + tid] = static_cast<float>(sc);
@@ -338,13 +435,14 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v
   for (int t = tid; t < D * 2; t += 256) {
     const int c = t >> 1, half = t & 1;
     const double sc = vsc[c], inv = 1.0 / sc;
+    const float inv32 = static_cast<float>(inv);
     uint32_t w[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) w[i] = 0u;
 #pragma unroll 8
     for (int i = 0; i < 32; ++i) {
       const int r = half * 32 + i;
-      const uint8_t code = e4m3_div(to_f64<T>(vraw[r * D + c]), sc, inv);
+      const uint8_t code = e4m3_div_fast(to_f32<T>(vraw[r * D + c]), sc, inv, inv32);
       w[i >> 2] |= static_cast<uint32_t>(code) << (8 * (i & 3));
     }
     uint8_t* vdst = v_codes + (static_cast<int64_t>(bh) * D + c) * Np + n0 + half * 32;
@@ -362,9 +460,13 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v
     __syncthreads();
     double acc = 0.0;
     if (r < rows) {
-#pragma unroll 8
-      for (int c = qq * (D / 4); c < (qq + 1) * (D / 4); ++c)
-        acc = fma(qmu[c], to_f64<T>(kraw[r * D + c]) - kmu[c], acc);
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent FMA chains (latency)
+#pragma unroll
+      for (int c = 0; c < D / 4; ++c) {
+        const int cc = qq * (D / 4) + c;
+        a4[c & 3] = fma(qmu[cc], static_cast<double>(to_f32<T>(kraw[r * D + cc])) - kmu[cc], a4[c & 3]);
+      }
+      acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
     }
     acc += __shfl_xor_sync(0xffffffffu, acc, 1);
     acc += __shfl_xor_sync(0xffffffffu, acc, 2);

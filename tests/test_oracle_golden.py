@@ -153,3 +153,33 @@ def test_live_reference_on_fresh_seed(lpattn):
     ours = oc.attention_quantized(q, k, v, oc.AttentionConfig(seq_len=160, head_dim=64, causal=True))
     np.testing.assert_allclose(ours.output, ref.output, rtol=0, atol=1e-12)
     assert ours.mma_invocations == ref.mma_invocations
+
+
+@pytest.mark.parametrize("case", ["exact_ties", "huge_offsets", "zeros_subnormals"])
+def test_oracle_prepass_edges_vs_live_reference(lpattn, case):
+    """The oracle's quantizers equal the reference's on the adversarial inputs the GPU prepass is
+    tested with (tests/test_gpu_prepass_edges.py): ties, huge offsets, zeros, subnormals."""
+    from lpattn import quantization as rq
+    from edge_inputs import CASES
+    q, k, v, smoothing = CASES[case]()
+    h, n, d = q.shape
+    cfg = oc.AttentionConfig(seq_len=n, head_dim=d, num_heads=h, smoothing=smoothing)
+    for hh in range(h):
+        ours = oc.prepass(q[hh], k[hh], v[hh], cfg)
+        qs, ks = (rq.smooth_q(q[hh])[0], rq.smooth_k(k[hh])[0]) if smoothing else (
+            q[hh].astype(np.float64), k[hh].astype(np.float64))
+        npad = -(-n // 64) * 64
+        ksp = np.zeros((npad, d))
+        ksp[:n] = ks
+        vp = np.zeros((npad, d))
+        vp[:n] = v[hh]
+        for j in range(npad // 64):
+            kb = rq.quantize_int_block(ksp[j * 64:(j + 1) * 64])
+            assert np.array_equal(ours.k_codes[j * 64:(j + 1) * 64], kb.codes) and ours.k_scale[j] == kb.scale
+            vb = rq.quantize_v_per_channel(vp[j * 64:(j + 1) * 64], 4.5)
+            assert np.array_equal(ours.v_codes[j * 64:(j + 1) * 64], vb.codes)
+            assert np.array_equal(ours.v_scale[j], vb.scales)
+        for i in range(-(-n // 128)):
+            qb = rq.quantize_int_block(qs[i * 128:min((i + 1) * 128, n)])
+            assert np.array_equal(ours.q_codes[i * 128:min((i + 1) * 128, n)], qb.codes)
+            assert ours.q_scale[i] == qb.scale
