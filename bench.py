@@ -321,14 +321,16 @@ def run_ours(a):
         src = (xq, xk, xv) if ulysses else (q, k, v)
         hq, hk, hv = (t.cpu().pin_memory() for t in src)
         ho = torch.empty(src[0].shape, dtype=out.dtype, pin_memory=True)
+        pipe = None if ulysses else sa.HostPipeline(1, Ul, Ul // group, N, D, torch.bfloat16, dev,
+                                                    is_causal=a.causal, pv_accum=a.pv_accum, chunks=16)
 
         def e2e_step():
-            dq, dk, dv = (h.to(dev, non_blocking=True) for h in (hq, hk, hv))
             if ulysses:
+                dq, dk, dv = (h.to(dev, non_blocking=True) for h in (hq, hk, hv))
                 r = parallel.ulysses_sageattn(dq, dk, dv, a.causal, None, pv_accum=a.pv_accum, quant=qt)
-            else:
-                r = sa.sageattn(dq, dk, dv, "HND", a.causal, None, pv_accum=a.pv_accum, quant=qt, out=out)
-            ho.copy_(r, non_blocking=True)
+                ho.copy_(r, non_blocking=True)
+            else:  # public host API: chunked copies in both directions overlapped with the kernels
+                pipe(hq, hk, hv, ho)
 
         for _ in range(2):
             e2e_step()

@@ -8,12 +8,12 @@ Public API:
 """
 
 from .config import TABLE2_PAIRS, AttentionConfig, RangeConfig, RangeConfigError
-from .api import (QuantizedTensors, RunReport, attention_quantized, compare, new_report, quantize,
-                  sageattn)
+from .api import (HostPipeline, QuantizedTensors, RunReport, attention_quantized, compare, new_report,
+                  quantize, sageattn, sageattn_host)
 
 __version__ = "1.0.0"
 __all__ = [
-    "sageattn", "attention_quantized", "quantize", "compare", "new_report",
+    "sageattn", "sageattn_host", "HostPipeline", "attention_quantized", "quantize", "compare", "new_report",
     "AttentionConfig", "RangeConfig", "RangeConfigError", "TABLE2_PAIRS",
     "QuantizedTensors", "RunReport",
 ]

@@ -149,6 +149,88 @@ def sageattn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, tensor_layout: s
     return (out, qt) if return_quant else out
 
 
+class HostPipeline:
+    """`sageattn` on pinned HOST tensors with the copies overlapped with the kernels.
+
+    The (batch, kv-head) units are cut into `chunks` (whole GQA groups, so every chunk is an
+    independent attention problem: smoothing statistics are per head); chunk i's host->device
+    copy, prepass + attention and device->host copy run on three streams through a ring of
+    `depth` device buffer sets, so PCIe traffic in both directions overlaps the tensor cores.
+    Inputs [B, H, N, D] (HND, contiguous, pinned); the output is written into `out` (pinned).
+    The caller's current stream is ordered after the last copy-back.
+    """
+
+    def __init__(self, B, Hq, Hkv, N, D, dtype=torch.bfloat16, device="cuda", *, is_causal=False,
+                 sm_scale=None, pv_accum="fp16", chunks=8, depth=2, **kw):
+        if Hq % Hkv:
+            raise ValueError("heads_q must be a multiple of heads_kv")
+        self.B, self.Hq, self.Hkv, self.N, self.D = B, Hq, Hkv, N, D
+        self.group = Hq // Hkv
+        self.device = torch.device(device)
+        self.causal, self.sm_scale, self.pv_accum, self.kw = is_causal, sm_scale, pv_accum, kw
+        units = B * Hkv
+        self.cu = -(-units // max(1, min(chunks, units)))  # kv units per chunk
+        self.spans = [(u, min(units, u + self.cu)) for u in range(0, units, self.cu)]
+        self.depth = max(1, min(depth, len(self.spans)))
+        g, cu = self.group, self.cu
+        mk = lambda h: torch.empty(1, h, N, D, dtype=dtype, device=self.device)  # noqa: E731
+        self.bufs = [(mk(cu * g), mk(cu), mk(cu), mk(cu * g)) for _ in range(self.depth)]
+        prob = _problem(1, cu * g, cu, N, D, causal=is_causal, pv_accum=pv_accum, sm_scale=sm_scale,
+                        smoothing=kw.get("smooth", True), qk_bits=kw.get("qk_bits", 8),
+                        p_r=kw.get("p_r", 224.0), v_r=kw.get("v_r", 4.5))
+        self.quant = [alloc_quant(prob, self.device) for _ in range(self.depth)]
+        self.h2d, self.comp, self.d2h = (torch.cuda.Stream(self.device) for _ in range(3))
+        ev = lambda: [torch.cuda.Event() for _ in range(self.depth)]  # noqa: E731
+        self.ev_in, self.ev_comp, self.ev_out = ev(), ev(), ev()
+
+    def __call__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
+        B, Hq, Hkv, N, D, g = self.B, self.Hq, self.Hkv, self.N, self.D, self.group
+        for t, h in ((q, Hq), (k, Hkv), (v, Hkv), (out, Hq)):
+            if t.is_cuda or tuple(t.shape) != (B, h, N, D) or not t.is_contiguous():
+                raise ValueError("HostPipeline takes contiguous [B, H, N, D] host tensors")
+        qf, kf, vf, of = (t.view(-1, N, D) for t in (q, k, v, out))
+        caller = torch.cuda.current_stream(self.device)
+        self.h2d.wait_stream(caller)
+        for i, (u0, u1) in enumerate(self.spans):
+            s = i % self.depth
+            dq, dk, dv, do = self.bufs[s]
+            n = u1 - u0
+            with torch.cuda.stream(self.h2d):
+                if i >= self.depth:
+                    self.h2d.wait_event(self.ev_out[s])  # buffer set s copied back
+                dq[0, :n * g].copy_(qf[u0 * g:u1 * g], non_blocking=True)
+                dk[0, :n].copy_(kf[u0:u1], non_blocking=True)
+                dv[0, :n].copy_(vf[u0:u1], non_blocking=True)
+                self.ev_in[s].record(self.h2d)
+            with torch.cuda.stream(self.comp):
+                self.comp.wait_event(self.ev_in[s])
+                if n == self.cu:
+                    sageattn(dq, dk, dv, "HND", self.causal, self.sm_scale, pv_accum=self.pv_accum, out=do,
+                             quant=self.quant[s], stream=self.comp, **self.kw)
+                else:  # ragged last chunk
+                    sageattn(dq[:, :n * g], dk[:, :n], dv[:, :n], "HND", self.causal, self.sm_scale,
+                             pv_accum=self.pv_accum, out=do[:, :n * g], stream=self.comp, **self.kw)
+                self.ev_comp[s].record(self.comp)
+            with torch.cuda.stream(self.d2h):
+                self.d2h.wait_event(self.ev_comp[s])
+                of[u0 * g:u1 * g].copy_(do[0, :n * g], non_blocking=True)
+                self.ev_out[s].record(self.d2h)
+        caller.wait_stream(self.d2h)
+        return out
+
+
+def sageattn_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, is_causal: bool = False,
+                  sm_scale: Optional[float] = None, *, out: Optional[torch.Tensor] = None, chunks: int = 8,
+                  **kw) -> torch.Tensor:
+    """One-shot `HostPipeline` call: pinned HND host tensors in, pinned host output out."""
+    B, Hq, N, D = q.shape
+    pipe = HostPipeline(B, Hq, k.shape[1], N, D, q.dtype, is_causal=is_causal, sm_scale=sm_scale, chunks=chunks,
+                        **kw)
+    if out is None:
+        out = torch.empty(q.shape, dtype=q.dtype, pin_memory=True)
+    return pipe(q, k, v, out)
+
+
 def new_report(device) -> torch.Tensor:
     """Device RunReport buffer: overflow count, min/max delta_P as float bits (see sa2pp_report)."""
     r = torch.zeros(4, dtype=torch.int32, device=device)

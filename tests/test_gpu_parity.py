@@ -201,3 +201,17 @@ def test_quantize_only_matches_sageattn_prepass():
     torch.cuda.synchronize()
     assert np.array_equal(qt.q_codes[0].cpu().numpy()[:, :200], g["q_codes"])
     assert np.array_equal(qt.k_codes[0].cpu().numpy(), g["k_codes"])
+
+
+@pytest.mark.parametrize("causal,hkv", [(False, 6), (True, 2)])
+def test_host_pipeline_equals_device_call(causal, hkv):
+    """sageattn_host / HostPipeline (chunked H2D, kernels, D2H on three streams) is bit-identical to
+    sageattn on device tensors, including a ragged last chunk and GQA groups."""
+    g = torch.Generator().manual_seed(7)
+    q = torch.randn(2, 6, 700, 128, generator=g).bfloat16().pin_memory()
+    k = torch.randn(2, hkv, 700, 128, generator=g).bfloat16().pin_memory()
+    v = torch.randn(2, hkv, 700, 128, generator=g).bfloat16().pin_memory()
+    out = sa.sageattn_host(q, k, v, causal, chunks=5)
+    torch.cuda.synchronize()
+    ref = sa.sageattn(q.cuda(), k.cuda(), v.cuda(), "HND", causal).cpu()
+    assert torch.equal(out, ref)
