@@ -173,22 +173,6 @@ __device__ __forceinline__ double div_rint(double x, double scale, double inv) {
 }
 
 
-// INT8/INT4 code of (v - mu) / scale (FP64 in the reference, quantization.py:151-160), fast path.
-// x32 = (v - mu_hi) - mu_lo and q = x32 * fl32(1/scale) in FP32 stay within 4e-5 of the exact
-// quotient whenever |mu| <= 2^16 * amax (the caller checks this per tile), so unless q is within 1e-4
-// of a rounding tie its RNE (magic-number add, exact for |q| < 2^22) is the reference's code; near a
-// tie the FP64 path decides.  No FP64 or conversion (XU) instruction on the common path.
-__device__ __forceinline__ int int_code_fast(float v, float mu_hi, float mu_lo, double mu, float inv32,
-                                             double scale, double inv64, int qmax) {
-  const float x = (v - mu_hi) - mu_lo;
-  const float q = x * inv32;
-  const float t = q + 12582912.0f;  // 1.5 * 2^23
-  const float r = t - 12582912.0f;
-  int c = __float_as_int(t) - 0x4B400000;
-  if (fabsf(fabsf(q - r) - 0.5f) < 1e-4f) c = static_cast<int>(div_rint(static_cast<double>(v) - mu, scale, inv64));
-  return min(max(c, -qmax), qmax);
-}
-
 // E4M3 code of x / scale, bit-identical to encoding the correctly rounded FP64 quotient: the
 // reciprocal product is used unless it sits within 1e-9 (relative to the grid step) of an E4M3
 // rounding boundary, in which case the exact quotient is encoded.
@@ -205,25 +189,28 @@ __device__ __forceinline__ uint8_t e4m3_div(double x, double scale, double inv) 
 }
 
 
-// E4M3 code of v / scale for the V quantizer, fast path.  q = v * fl32(1/scale) in FP32 is within
-// 2 f32 ulps of the exact quotient (two roundings of 2^-24), so unless q sits within 64 ulps of an
-// E4M3 rounding tie the hardware RNE-satfinite conversion of q gives the same code as encoding the
-// correctly rounded FP64 quotient (numerics.py:152-182); near a tie the exact FP64 path decides.
-__device__ __forceinline__ uint8_t e4m3_div_fast(float v, double scale, double inv64, float inv32) {
+
+// Branch-free halves of the fast paths: the code assuming no tie, and whether the element is near
+// one.  Callers OR the flags over a batch and redo the whole batch exactly in the rare case, so the
+// common path carries no per-element divergence/reconvergence.
+__device__ __forceinline__ int int_code_nt(float v, float mu_hi, float mu_lo, float inv32, int qmax, bool& tie) {
+  const float q = ((v - mu_hi) - mu_lo) * inv32;
+  const float t = q + 12582912.0f;  // 1.5 * 2^23
+  tie |= fabsf(fabsf(q - (t - 12582912.0f)) - 0.5f) < 1e-4f;
+  return min(max(__float_as_int(t) - 0x4B400000, -qmax), qmax);
+}
+__device__ __forceinline__ int int_code_exact(float v, double mu, double scale, double inv64, int qmax) {
+  return min(max(static_cast<int>(div_rint(static_cast<double>(v) - mu, scale, inv64)), -qmax), qmax);
+}
+__device__ __forceinline__ uint32_t e4m3_nt(float v, float inv32, bool& tie) {
   const float q = v * inv32;
   const uint32_t a = __float_as_uint(q) & 0x7FFFFFFFu;
-  bool near_tie;
-  if (a >= 0x3C800000u) {  // |q| >= 2^-6: normal E4M3, 20 discarded mantissa bits
-    const uint32_t d = a & 0xFFFFFu;
-    near_tie = d > 0x80000u - 64u && d < 0x80000u + 64u;
-  } else {  // subnormal E4M3: step 2^-9, ties at odd multiples of 2^-10 (q * 512 is exact)
-    const float y = __uint_as_float(a) * 512.0f;
-    near_tie = fabsf((y - truncf(y)) - 0.5f) < 1e-4f;
-  }
-  if (near_tie) return e4m3_div(static_cast<double>(v), scale, inv64);
+  const uint32_t d = a & 0xFFFFFu;
+  const float y = __uint_as_float(a) * 512.0f;
+  tie |= a >= 0x3C800000u ? (d > 0x80000u - 64u && d < 0x80000u + 64u) : (fabsf((y - truncf(y)) - 0.5f) < 1e-4f);
   uint16_t r;
   asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(0.0f), "f"(q));
-  return static_cast<uint8_t>(r & 0xFF);
+  return r & 0xFFu;
 }
 
 // ------------------------------------------------------------------ pass 2: Q tiles
@@ -280,7 +267,7 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(InView qv, int Hq, int 
   }
   const double inv = 1.0 / scale;
   const float inv32 = static_cast<float>(inv);
-  const bool fast = mumax <= 65536.0 * amax;  // the error bound of int_code_fast
+  const bool fast = mumax <= 65536.0 * amax;  // the error bound of int_code_nt
   float mu_hi[VEC], mu_lo[VEC];
 #pragma unroll
   for (int i = 0; i < VEC; ++i) {
@@ -295,16 +282,18 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(InView qv, int Hq, int 
     if (n < n1) {
       const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(qv, b, h, n) + c8 * VEC);
       const T* e = reinterpret_cast<const T*>(&raw);
+      bool tie = !fast;
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        const float v = to_f32<T>(e[i]);
-        int c;
-        if (fast) {
-          c = int_code_fast(v, mu_hi[i], mu_lo[i], mup[i], inv32, scale, inv, qmax);
-        } else {
-          c = min(max(static_cast<int>(div_rint(static_cast<double>(v) - mup[i], scale, inv)), -qmax), qmax);
-        }
-        w[i >> 2] |= (static_cast<uint32_t>(c) & 0xFFu) << (8 * (i & 3));
+      for (int i = 0; i < VEC; ++i)
+        w[i >> 2] |= (static_cast<uint32_t>(int_code_nt(to_f32<T>(e[i]), mu_hi[i], mu_lo[i], inv32, qmax, tie)) & 0xFFu)
+                     << (8 * (i & 3));
+      if (tie) {  // rare: near a rounding tie or |mu| >> amax -> the FP64 quotient for the batch
+#pragma unroll
+        for (int i = 0; i < VEC / 4; ++i) w[i] = 0u;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i)
+          w[i >> 2] |= (static_cast<uint32_t>(int_code_exact(to_f32<T>(e[i]), mup[i], scale, inv, qmax)) & 0xFFu)
+                       << (8 * (i & 3));
       }
     }
     int8_t* o = dst + static_cast<int64_t>(n) * D + c8 * VEC;
@@ -393,7 +382,7 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v
   const double kscale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
   const double kinv = 1.0 / kscale;
   const float kinv32 = static_cast<float>(kinv);
-  const bool kfast = mumax <= 65536.0 * amax;  // the error bound of int_code_fast
+  const bool kfast = mumax <= 65536.0 * amax;  // the error bound of int_code_nt
 
   // ---- K codes: 8 consecutive channels per thread-iteration, one 8-byte store
   int8_t* kdst = k_codes + (static_cast<int64_t>(bh) * Np + n0) * D;
@@ -401,16 +390,22 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v
     const int r = g / (D / 8), c = (g % (D / 8)) * 8;
     uint32_t w[2] = {0u, 0u};
     if (r < rows) {
+      const uint4 raw = *reinterpret_cast<const uint4*>(kraw + r * D + c);  // 8 channels (16-bit T)
+      float v[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float v = to_f32<T>(kraw[r * D + c + i]);
-        int q;
-        if (kfast) {
-          q = int_code_fast(v, kmu_hi[c + i], kmu_lo[c + i], kmu[c + i], kinv32, kscale, kinv, qmax);
-        } else {
-          q = min(max(static_cast<int>(div_rint(static_cast<double>(v) - kmu[c + i], kscale, kinv)), -qmax), qmax);
-        }
-        w[i >> 2] |= (static_cast<uint32_t>(q) & 0xFFu) << (8 * (i & 3));
+      for (int i = 0; i < 8; ++i) v[i] = sizeof(T) == 2 ? to_f32<T>(reinterpret_cast<const T*>(&raw)[i])
+                                                         : to_f32<T>(kraw[r * D + c + i]);
+      bool tie = !kfast;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        w[i >> 2] |= (static_cast<uint32_t>(int_code_nt(v[i], kmu_hi[c + i], kmu_lo[c + i], kinv32, qmax, tie)) & 0xFFu)
+                     << (8 * (i & 3));
+      if (tie) {  // rare: near a rounding tie or |mu| >> amax -> the FP64 quotient for the batch
+        w[0] = w[1] = 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          w[i >> 2] |= (static_cast<uint32_t>(int_code_exact(v[i], kmu[c + i], kscale, kinv, qmax)) & 0xFFu)
+                       << (8 * (i & 3));
       }
     }
     *reinterpret_cast<uint2*>(kdst + static_cast<int64_t>(r) * D + c) = make_uint2(w[0], w[1]);
@@ -439,11 +434,17 @@ __global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v
     uint32_t w[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) w[i] = 0u;
-#pragma unroll 8
-    for (int i = 0; i < 32; ++i) {
-      const int r = half * 32 + i;
-      const uint8_t code = e4m3_div_fast(to_f32<T>(vraw[r * D + c]), sc, inv, inv32);
-      w[i >> 2] |= static_cast<uint32_t>(code) << (8 * (i & 3));
+    bool tie = false;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      w[i >> 2] |= e4m3_nt(to_f32<T>(vraw[(half * 32 + i) * D + c]), inv32, tie) << (8 * (i & 3));
+    if (tie) {  // rare: some element near an E4M3 rounding tie -> the exact FP64 encoder for all 32
+#pragma unroll
+      for (int i = 0; i < 8; ++i) w[i] = 0u;
+#pragma unroll 4
+      for (int i = 0; i < 32; ++i)
+        w[i >> 2] |= static_cast<uint32_t>(e4m3_div(to_f64<T>(vraw[(half * 32 + i) * D + c]), sc, inv))
+                     << (8 * (i & 3));
     }
     uint8_t* vdst = v_codes + (static_cast<int64_t>(bh) * D + c) * Np + n0 + half * 32;
     *reinterpret_cast<uint4*>(vdst) = make_uint4(w[0], w[1], w[2], w[3]);
