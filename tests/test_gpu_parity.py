@@ -215,3 +215,44 @@ def test_host_pipeline_equals_device_call(causal, hkv):
     torch.cuda.synchronize()
     ref = sa.sageattn(q.cuda(), k.cuda(), v.cuda(), "HND", causal).cpu()
     assert torch.equal(out, ref)
+
+
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+def test_ragged_lengths_vs_exact(d, causal):
+    """Sequence lengths around the 64-key block and 128-query tile edges (attention.py:223-229)."""
+    g = torch.Generator(device="cuda").manual_seed(d + causal)
+    for n in (1, 2, 63, 64, 65, 127, 128, 129, 191, 257):
+        q, k, v = (torch.randn(1, 3, n, d, device="cuda", generator=g) for _ in range(3))
+        v = v + 1.5  # keep the outputs away from zero so relative L1 is meaningful
+        o = sa.sageattn(q, k, v, is_causal=causal)
+        ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, is_causal=causal)
+        cos, l1, _ = sa.compare(ref.double().cpu().numpy(), o.double().cpu().numpy())
+        assert cos >= 0.999 and l1 <= 2e-2, (n, cos, l1)
+        assert torch.isfinite(o).all()
+
+
+def test_nhd_strided_views_and_fp16():
+    """Non-contiguous NHD views (a slice of a packed QKV tensor) in fp16."""
+    g = torch.Generator(device="cuda").manual_seed(9)
+    qkv = torch.randn(2, 300, 3, 4, 64, device="cuda", generator=g).half()
+    q, k, v = qkv[:, :, 0], qkv[:, :, 1], qkv[:, :, 2]  # [B, N, H, D] views, token stride 3*4*64
+    o = sa.sageattn(q, k, v, "NHD", False)
+    o2 = sa.sageattn(q.contiguous(), k.contiguous(), v.contiguous(), "NHD", False)
+    torch.cuda.synchronize()
+    assert torch.equal(o, o2)
+    ref = torch.nn.functional.scaled_dot_product_attention(*(t.transpose(1, 2).float() for t in (q, k, v)))
+    cos, _, _ = sa.compare(ref.transpose(1, 2).double().cpu().numpy(), o.double().cpu().numpy())
+    assert cos >= 0.999
+
+
+def test_rejects_unsupported_inputs():
+    q = torch.randn(1, 2, 64, 96, device="cuda")
+    with pytest.raises(ValueError):
+        sa.sageattn(q, q, q)  # head_dim 96 is not built
+    with pytest.raises(ValueError):
+        sa.sageattn(q.cpu(), q.cpu(), q.cpu())  # no CPU fallback
+    q = torch.randn(1, 6, 64, 64, device="cuda")
+    k = torch.randn(1, 4, 64, 64, device="cuda")
+    with pytest.raises(ValueError):
+        sa.sageattn(q, k, k)  # 6 query heads over 4 KV heads
