@@ -17,6 +17,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cstdint>
+#include <type_traits>
 
 #include "sa2pp_internal.h"
 
@@ -89,14 +90,42 @@ __global__ void __launch_bounds__(256) channel_sums_kernel(InView qv, InView kv,
   double hi[VEC], lo[VEC];
 #pragma unroll
   for (int i = 0; i < VEC; ++i) hi[i] = lo[i] = 0.0;
-  for (int n = n_begin + r0; n < n_end; n += ROWS_PER_PASS) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(v, b, hh, n) + c8 * VEC);
-    const T* e = reinterpret_cast<const T*>(&raw);
+  // The next U rows stream into shared memory with cp.async (no registers held, so the compiler
+  // cannot sink the loads behind the FP64 chain) while the current U rows are summed.  Every thread
+  // reads back only its own copies: cp.async.wait_group is the only synchronisation.  Rows past the
+  // chunk are zero-filled, which adds exactly nothing.
+  constexpr int U = 4;
+  __shared__ __align__(16) uint4 smem_cs[2 * U * 256];  // 32 KB; reused by the combine below
+  auto issue = [&](int n0, int slot) {
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) dd_add(hi[i], lo[i], to_f64<T>(e[i]));
+    for (int u = 0; u < U; ++u) {
+      const int n = n0 + u * ROWS_PER_PASS;
+      const T* src = row_ptr<T>(v, b, hh, n < n_end ? n : n_begin) + c8 * VEC;
+      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&smem_cs[(slot * U + u) * 256 + threadIdx.x]));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n < n_end ? 16 : 0)
+                   : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(n_begin + r0, 0);
+  int slot = 0;
+  for (int n = n_begin + r0; n < n_end; n += U * ROWS_PER_PASS) {
+    issue(n + U * ROWS_PER_PASS, slot ^ 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint4 raw = smem_cs[(slot * U + u) * 256 + threadIdx.x];
+      const T* e = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) dd_add(hi[i], lo[i], to_f64<T>(e[i]));
+    }
+    slot ^= 1;
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
   // Fixed-order combine of the ROWS_PER_PASS row-groups through shared memory.
-  __shared__ double2 red[256 * VEC];
+  static_assert(sizeof(double2) * 256 * VEC <= sizeof(smem_cs), "combine buffer fits the staging buffer");
+  double2* red = reinterpret_cast<double2*>(smem_cs);
 #pragma unroll
   for (int i = 0; i < VEC; ++i) red[threadIdx.x * VEC + i] = make_double2(hi[i], lo[i]);
   __syncthreads();
@@ -282,18 +311,23 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(InView qv, int Hq, int 
     if (n < n1) {
       const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(qv, b, h, n) + c8 * VEC);
       const T* e = reinterpret_cast<const T*>(&raw);
-      bool tie = !fast;
+      uint32_t tmask = fast ? 0u : (1u << VEC) - 1u;
 #pragma unroll
-      for (int i = 0; i < VEC; ++i)
+      for (int i = 0; i < VEC; ++i) {
+        bool tie = false;
         w[i >> 2] |= (static_cast<uint32_t>(int_code_nt(to_f32<T>(e[i]), mu_hi[i], mu_lo[i], inv32, qmax, tie)) & 0xFFu)
                      << (8 * (i & 3));
-      if (tie) {  // rare: near a rounding tie or |mu| >> amax -> the FP64 quotient for the batch
+        tmask |= static_cast<uint32_t>(tie) << i;
+      }
+      while (tmask) {  // rare: near a rounding tie or |mu| >> amax -> the FP64 quotient per element
+        const int i = __ffs(tmask) - 1;
+        tmask &= tmask - 1u;
+        const float x = to_f32<T>(row_ptr<T>(qv, b, h, n)[c8 * VEC + i]);
+        const uint32_t code = static_cast<uint32_t>(int_code_exact(x, mup[i], scale, inv, qmax)) & 0xFFu;
+        const int sh = 8 * (i & 3);
 #pragma unroll
-        for (int i = 0; i < VEC / 4; ++i) w[i] = 0u;
-#pragma unroll
-        for (int i = 0; i < VEC; ++i)
-          w[i >> 2] |= (static_cast<uint32_t>(int_code_exact(to_f32<T>(e[i]), mup[i], scale, inv, qmax)) & 0xFFu)
-                       << (8 * (i & 3));
+        for (int k = 0; k < VEC / 4; ++k)
+          if (k == (i >> 2)) w[k] = (w[k] & ~(0xFFu << sh)) | (code << sh);
       }
     }
     int8_t* o = dst + static_cast<int64_t>(n) * D + c8 * VEC;
@@ -306,176 +340,334 @@ __global__ void __launch_bounds__(256) quantize_q_kernel(InView qv, int Hq, int 
 }
 
 // ------------------------------------------------------------------ pass 3: K/V blocks
-// One CTA (256 threads) per 64-key block of one (b, hkv).  The raw K and V tiles are staged in
-// shared memory once; everything else works from there.
-//   k_codes  [B, Hkv, Np, D]          int8
-//   v_codes  [B, Hkv, D, Np]          E4M3, transposed so the PV operand is K-major
+// One CTA (256 threads) per 64-key block of one (b, hkv).  Thread (rg, c8) holds channels
+// [8*c8, 8*c8+8) of the RT consecutive keys [rg*RT, rg*RT+RT) of both K and V in registers, so the
+// block is read from HBM exactly once and every output is produced from registers:
+//   k_codes  [B, Hkv, Np, D]          int8, 8-byte stores straight from registers
+//   v_codes  [B, Hkv, D, Np]          E4M3, transposed through a swizzled 64-byte-per-channel smem tile
 //   kv_meta  [B, Hkv, nKB, 4 + D]     f32 {dK, 0, 0, 0, dV[0..D)}
 //   bias     [B, Hq, Np]              f32 q_mean . Ks_j ; bias_l2 = bias * sm_scale * log2(e)
+// Per-channel statistics (K min/max, V |max|) are reduced across the row groups with shuffles and
+// across warps through shared memory; the block scalars need two CTA barriers, the transpose a third.
+// Rare-path encoders kept out of line so the unrolled fast paths stay small in the i-cache.
+__device__ __noinline__ uint32_t k_codes_exact8(const float* x, const double* mu, double scale, double inv, int qmax,
+                                                 uint32_t* w1) {
+  uint32_t w0 = 0u, hi = 0u;
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t code = static_cast<uint32_t>(int_code_exact(x[i], mu[i], scale, inv, qmax)) & 0xFFu;
+    if (i < 4) {
+      w0 |= code << (8 * i);
+    } else {
+      hi |= code << (8 * (i - 4));
+    }
+  }
+  *w1 = hi;
+  return w0;
+}
+__device__ __noinline__ uint8_t v_code_exact(float x, double sc) {
+  return e4m3_div(static_cast<double>(x), sc, 1.0 / sc);
+}
+
+template <typename T>
+struct KvTile {
+  static constexpr int kWords = 8 * static_cast<int>(sizeof(T)) / 4;  // 32-bit words per 8 channels
+  uint32_t w[kWords];
+  __device__ __forceinline__ float get(int i) const {
+    if constexpr (sizeof(T) == 4) {
+      return __uint_as_float(w[i]);
+    } else if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+      return __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
+    } else {
+      const __half2 h = *reinterpret_cast<const __half2*>(&w[i >> 1]);
+      return (i & 1) ? __high2float(h) : __low2float(h);
+    }
+  }
+  __device__ __forceinline__ float2 get2(int i) const { return make_float2(get(i), get(i + 1)); }
+};
+
 template <typename T, int D>
 __host__ __device__ constexpr int kv_smem_bytes() {
-  return 2 * 64 * D * static_cast<int>(sizeof(T)) + 3 * D * 8 + 2 * D * 4 + 64;
+  return 3 * 8 * D * 4 + D * 64 + D * 8 + D * 4 + 64;
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(256) quantize_kv_kernel(InView kv_in, InView v_in, int Hq, int Hkv, int N, int Np,
-                                                          int n_kb, int qmax, double v_r, int smoothing,
-                                                          double sm_scale_log2, const double* __restrict__ means,
-                                                          int Ht, int8_t* __restrict__ k_codes,
-                                                          uint8_t* __restrict__ v_codes, float* __restrict__ kv_meta,
-                                                          double* __restrict__ kv_scale64, float* __restrict__ bias,
-                                                          float* __restrict__ bias_l2) {
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int NV = 64 * D / VEC;  // 16-byte vectors per tile
+__global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InView v_in, int Hq, int Hkv, int N, int Np,
+                                                             int n_kb, int qmax, double v_r, int smoothing,
+                                                             double sm_scale_log2, const double* __restrict__ means,
+                                                             int Ht, int8_t* __restrict__ k_codes,
+                                                             uint8_t* __restrict__ v_codes, float* __restrict__ kv_meta,
+                                                             double* __restrict__ kv_scale64, float* __restrict__ bias,
+                                                             float* __restrict__ bias_l2) {
+  constexpr int LPR = D / 8;         // lanes per key row
+  constexpr int RPP = 256 / LPR;     // row groups per CTA
+  constexpr int RT = 64 / RPP;       // consecutive keys per thread (4 for D=128, 2 for D=64)
+  constexpr int UPR = 64 / RT;       // RT-byte units per 64-key V^T row
+  constexpr int NW = sizeof(T) == 4 ? 2 : 1;  // 16-byte loads per 8 channels
   extern __shared__ __align__(16) unsigned char kv_smem[];
-  T* kraw = reinterpret_cast<T*>(kv_smem);
-  T* vraw = kraw + 64 * D;
-  double* kmu = reinterpret_cast<double*>(kv_smem + 2 * 64 * D * sizeof(T));
-  double* qmu = kmu + D;
-  double* vsc = qmu + D;
-  float* kmu_hi = reinterpret_cast<float*>(vsc + D);
-  float* kmu_lo = kmu_hi + D;
-  __shared__ double scratch[8];
+  float* s_kmn = reinterpret_cast<float*>(kv_smem);  // [8 warps][D]
+  float* s_kmx = s_kmn + 8 * D;
+  float* s_vmx = s_kmx + 8 * D;
+  uint8_t* s_vt = reinterpret_cast<uint8_t*>(s_vmx + 8 * D);    // [D][64] swizzled E4M3 codes
+  double* s_vsc = reinterpret_cast<double*>(s_vt + D * 64);    // [D]
+  float* s_vinv = reinterpret_cast<float*>(s_vsc + D);         // [D]
+  double* s_red = reinterpret_cast<double*>(s_vinv + D);       // [4] amax, [4] |mu| max
   const int kb = blockIdx.x;
   const int bh = blockIdx.y;
   const int b = bh / Hkv, h = bh % Hkv;
   const int n0 = kb * 64;
   const int rows = min(64, N - n0);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c8 = tid % LPR, rg = tid / LPR;
+  const int c0 = c8 * 8;
 
-  // ---- stage the tiles (rows past N are zero: the reference pads after smoothing)
-  for (int i = tid; i < NV; i += 256) {
-    const int r = i / (D / VEC), c = (i % (D / VEC)) * VEC;
-    uint4 kvv = make_uint4(0, 0, 0, 0), vvv = make_uint4(0, 0, 0, 0);
-    if (r < rows) {
-      kvv = *reinterpret_cast<const uint4*>(row_ptr<T>(kv_in, b, h, n0 + r) + c);
-      vvv = *reinterpret_cast<const uint4*>(row_ptr<T>(v_in, b, h, n0 + r) + c);
+  // ---- load: RT rows x 8 channels of K and V (rows past N are zero: padding after smoothing)
+  KvTile<T> kt[RT], vt[RT];
+#pragma unroll
+  for (int rr = 0; rr < RT; ++rr) {
+    const int r = rg * RT + rr;
+#pragma unroll
+    for (int u = 0; u < NW; ++u) {
+      uint4 kx = make_uint4(0, 0, 0, 0), vx = make_uint4(0, 0, 0, 0);
+      if (r < rows) {
+        kx = __ldcs(reinterpret_cast<const uint4*>(row_ptr<T>(kv_in, b, h, n0 + r) + c0) + u);
+        vx = __ldcs(reinterpret_cast<const uint4*>(row_ptr<T>(v_in, b, h, n0 + r) + c0) + u);
+      }
+      kt[rr].w[4 * u] = kx.x; kt[rr].w[4 * u + 1] = kx.y; kt[rr].w[4 * u + 2] = kx.z; kt[rr].w[4 * u + 3] = kx.w;
+      vt[rr].w[4 * u] = vx.x; vt[rr].w[4 * u + 1] = vx.y; vt[rr].w[4 * u + 2] = vx.z; vt[rr].w[4 * u + 3] = vx.w;
     }
-    *reinterpret_cast<uint4*>(kraw + r * D + c) = kvv;
-    *reinterpret_cast<uint4*>(vraw + r * D + c) = vvv;
   }
-  if (tid < D) {
-    const double m = means[(static_cast<int64_t>(b) * Ht + Hq + h) * D + tid];
-    kmu[tid] = m;
-    kmu_hi[tid] = static_cast<float>(m);
-    kmu_lo[tid] = static_cast<float>(m - static_cast<double>(kmu_hi[tid]));
+  const double* kmu_g = means + (static_cast<int64_t>(b) * Ht + Hq + h) * D;
+
+  // ---- per-channel statistics over the block's valid rows
+  {
+    float mn[8], mx[8], va[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      mn[i] = INFINITY;
+      mx[i] = -INFINITY;
+      va[i] = 0.0f;
+    }
+#pragma unroll
+    for (int rr = 0; rr < RT; ++rr) {
+      const bool ok = rg * RT + rr < rows;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float x = kt[rr].get(i);
+        mn[i] = fminf(mn[i], ok ? x : INFINITY);
+        mx[i] = fmaxf(mx[i], ok ? x : -INFINITY);
+        va[i] = fmaxf(va[i], fabsf(vt[rr].get(i)));
+      }
+    }
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        mn[i] = fminf(mn[i], __shfl_xor_sync(0xffffffffu, mn[i], o));
+        mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
+        va[i] = fmaxf(va[i], __shfl_xor_sync(0xffffffffu, va[i], o));
+      }
+    }
+    if (lane < LPR) {
+      float* d0 = s_kmn + warp * D + c0;
+      float* d1 = s_kmx + warp * D + c0;
+      float* d2 = s_vmx + warp * D + c0;
+      *reinterpret_cast<float4*>(d0) = make_float4(mn[0], mn[1], mn[2], mn[3]);
+      *reinterpret_cast<float4*>(d0 + 4) = make_float4(mn[4], mn[5], mn[6], mn[7]);
+      *reinterpret_cast<float4*>(d1) = make_float4(mx[0], mx[1], mx[2], mx[3]);
+      *reinterpret_cast<float4*>(d1 + 4) = make_float4(mx[4], mx[5], mx[6], mx[7]);
+      *reinterpret_cast<float4*>(d2) = make_float4(va[0], va[1], va[2], va[3]);
+      *reinterpret_cast<float4*>(d2 + 4) = make_float4(va[4], va[5], va[6], va[7]);
+    }
   }
   __syncthreads();
 
-  // ---- K: smoothed block amax -> scale (quantization.py:151-160) from per-channel min/max
-  //      (fl64(k - mu) is monotone in k: same value as the element-wise FP64 max)
-  double amax = 0.0, mumax = 0.0;
-  {
-    constexpr int TPC = 256 / D;  // threads per channel
-    const int c = tid % D;
-    float mn = INFINITY, mx = -INFINITY;
-    for (int r = tid / D; r < rows; r += TPC) {
-      const float x = to_f32<T>(kraw[r * D + c]);
-      mn = fminf(mn, x);
-      mx = fmaxf(mx, x);
-    }
-    if (mx >= mn) amax = fmax(fabs(static_cast<double>(mx) - kmu[c]), fabs(static_cast<double>(mn) - kmu[c]));
-    mumax = fabs(kmu[c]);
-  }
-  amax = block_max_256(amax, scratch);
-  mumax = block_max_256(mumax, scratch);
-  const double kscale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
-  const double kinv = 1.0 / kscale;
-  const float kinv32 = static_cast<float>(kinv);
-  const bool kfast = mumax <= 65536.0 * amax;  // the error bound of int_code_nt
-
-  // ---- K codes: 8 consecutive channels per thread-iteration, one 8-byte store
-  int8_t* kdst = k_codes + (static_cast<int64_t>(bh) * Np + n0) * D;
-  for (int g = tid; g < 64 * D / 8; g += 256) {
-    const int r = g / (D / 8), c = (g % (D / 8)) * 8;
-    uint32_t w[2] = {0u, 0u};
-    if (r < rows) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(kraw + r * D + c);  // 8 channels (16-bit T)
-      float v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = sizeof(T) == 2 ? to_f32<T>(reinterpret_cast<const T*>(&raw)[i])
-                                                         : to_f32<T>(kraw[r * D + c + i]);
-      bool tie = !kfast;
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        w[i >> 2] |= (static_cast<uint32_t>(int_code_nt(v[i], kmu_hi[c + i], kmu_lo[c + i], kinv32, qmax, tie)) & 0xFFu)
-                     << (8 * (i & 3));
-      if (tie) {  // rare: near a rounding tie or |mu| >> amax -> the FP64 quotient for the batch
-        w[0] = w[1] = 0u;
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-          w[i >> 2] |= (static_cast<uint32_t>(int_code_exact(v[i], kmu[c + i], kscale, kinv, qmax)) & 0xFFu)
-                       << (8 * (i & 3));
-      }
-    }
-    *reinterpret_cast<uint2*>(kdst + static_cast<int64_t>(r) * D + c) = make_uint2(w[0], w[1]);
-  }
-
-  // ---- V: per-channel block max -> scale (quantization.py:178-188); |x| max is exact in f32
+  // ---- channel scalars: K smoothed amax (quantization.py:151-160; fl64(k - mu) is monotone in k, so
+  //      the channel min/max give the element-wise FP64 max), V scale (quantization.py:178-188)
   float* meta = kv_meta + (static_cast<int64_t>(bh) * n_kb + kb) * (4 + D);
   double* sc64 = kv_scale64 + (static_cast<int64_t>(bh) * n_kb + kb) * (1 + D);
   if (tid < D) {
-    float m = 0.0f;
-    for (int r = 0; r < rows; ++r) m = fmaxf(m, fabsf(to_f32<T>(vraw[r * D + tid])));
-    const double sc = m > 0.0f ? static_cast<double>(m) / v_r : 1.0;
-    vsc[tid] = sc;
+    float mn = INFINITY, mx = -INFINITY, va = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      mn = fminf(mn, s_kmn[w * D + tid]);
+      mx = fmaxf(mx, s_kmx[w * D + tid]);
+      va = fmaxf(va, s_vmx[w * D + tid]);
+    }
+    const double mu = kmu_g[tid];
+    double amax = 0.0;
+    if (mx >= mn) amax = fmax(fabs(static_cast<double>(mx) - mu), fabs(static_cast<double>(mn) - mu));
+    double mumax = fabs(mu);
+    const double sc = va > 0.0f ? static_cast<double>(va) / v_r : 1.0;
+    s_vsc[tid] = sc;
+    s_vinv[tid] = static_cast<float>(1.0 / sc);
     meta[4 + tid] = static_cast<float>(sc);
     sc64[1 + tid] = sc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      mumax = fmax(mumax, __shfl_xor_sync(0xffffffffu, mumax, o));
+    }
+    if (lane == 0) {
+      s_red[warp] = amax;
+      s_red[4 + warp] = mumax;
+    }
   }
+  __syncthreads();
+  double amax = s_red[0], mumax = s_red[4];
+#pragma unroll
+  for (int w = 1; w < D / 32; ++w) {
+    amax = fmax(amax, s_red[w]);
+    mumax = fmax(mumax, s_red[4 + w]);
+  }
+  const double kscale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
+  const double kinv = 1.0 / kscale;
+  const float kinv32 = static_cast<float>(kinv);
+  const bool kfast = mumax <= 65536.0 * amax;  // the error bound of the FP32 fast path
   if (tid < 4) meta[tid] = tid == 0 ? static_cast<float>(kscale) : 0.0f;
   if (tid == 0) sc64[0] = kscale;
-  __syncthreads();
 
-  // ---- V codes, transposed: thread -> (channel, 32-row half); 32 codes -> two 16-byte stores
-  for (int t = tid; t < D * 2; t += 256) {
-    const int c = t >> 1, half = t & 1;
-    const double sc = vsc[c], inv = 1.0 / sc;
-    const float inv32 = static_cast<float>(inv);
-    uint32_t w[8];
+  // ---- K codes: ((k - mu_hi) - mu_lo) * inv rounded with the 1.5*2^23 trick; the code is the low
+  //      byte of the rounded float's bits.  |q| <= qmax + 3e-5 under kfast, so no clamp is needed.
+  {
+    float2 mh[4], ml[4];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) w[i] = 0u;
-    bool tie = false;
-#pragma unroll
-    for (int i = 0; i < 32; ++i)
-      w[i >> 2] |= e4m3_nt(to_f32<T>(vraw[(half * 32 + i) * D + c]), inv32, tie) << (8 * (i & 3));
-    if (tie) {  // rare: some element near an E4M3 rounding tie -> the exact FP64 encoder for all 32
-#pragma unroll
-      for (int i = 0; i < 8; ++i) w[i] = 0u;
-#pragma unroll 4
-      for (int i = 0; i < 32; ++i)
-        w[i >> 2] |= static_cast<uint32_t>(e4m3_div(to_f64<T>(vraw[(half * 32 + i) * D + c]), sc, inv))
-                     << (8 * (i & 3));
+    for (int i = 0; i < 8; i += 2) {
+      const double2 m2 = *reinterpret_cast<const double2*>(kmu_g + c0 + i);
+      mh[i / 2] = make_float2(static_cast<float>(m2.x), static_cast<float>(m2.y));
+      ml[i / 2] = make_float2(static_cast<float>(m2.x - static_cast<double>(mh[i / 2].x)),
+                              static_cast<float>(m2.y - static_cast<double>(mh[i / 2].y)));
     }
-    uint8_t* vdst = v_codes + (static_cast<int64_t>(bh) * D + c) * Np + n0 + half * 32;
-    *reinterpret_cast<uint4*>(vdst) = make_uint4(w[0], w[1], w[2], w[3]);
-    *reinterpret_cast<uint4*>(vdst + 16) = make_uint4(w[4], w[5], w[6], w[7]);
+    const float2 inv2 = make_float2(kinv32, kinv32);
+    const float2 magic2 = make_float2(12582912.0f, 12582912.0f);
+    int8_t* kdst = k_codes + (static_cast<int64_t>(bh) * Np + n0 + rg * RT) * D + c0;
+#pragma unroll
+    for (int rr = 0; rr < RT; ++rr) {
+      uint32_t tb[8];
+      bool tie = !kfast;
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const float2 d = __fadd2_rn(__fadd2_rn(kt[rr].get2(i), make_float2(-mh[i / 2].x, -mh[i / 2].y)),
+                                    make_float2(-ml[i / 2].x, -ml[i / 2].y));
+        const float2 q = __fmul2_rn(d, inv2);
+        const float2 t = __fadd2_rn(q, magic2);
+        const float2 f = __fadd2_rn(q, __fadd2_rn(make_float2(-t.x, -t.y), magic2));  // q - round(q)
+        tie |= (fabsf(f.x) > 0.4999f) | (fabsf(f.y) > 0.4999f);
+        tb[i] = __float_as_uint(t.x);
+        tb[i + 1] = __float_as_uint(t.y);
+      }
+      uint32_t w0 = __byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410);
+      uint32_t w1 = __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410);
+      const bool valid = rg * RT + rr < rows;
+      if (tie && valid) {  // rare: near a rounding tie or |mu| >> amax -> FP64 quotients for these 8
+        float x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = kt[rr].get(i);
+        w0 = k_codes_exact8(x, kmu_g + c0, kscale, kinv, qmax, &w1);
+      }
+      if (!valid) w0 = w1 = 0u;
+      *reinterpret_cast<uint2*>(kdst + rr * D) = make_uint2(w0, w1);
+    }
   }
 
-  // ---- bias for every query head sharing this KV head: b_j = q_mean . Ks_j (attention.py:288-289)
-  const int group = Hq / Hkv;
-  const int r = tid >> 2, qq = tid & 3;  // row, quarter of the channels
-  for (int g = 0; g < group; ++g) {
-    const int hq = h * group + g;
-    __syncthreads();
-    if (tid < D) qmu[tid] = smoothing ? means[(static_cast<int64_t>(b) * Ht + hq) * D + tid] : 0.0;
-    __syncthreads();
-    double acc = 0.0;
-    if (r < rows) {
-      double a4[4] = {0.0, 0.0, 0.0, 0.0};  // four independent FMA chains (latency)
+  // ---- V codes (E4M3, RNE, satfinite): tie test = the codes of q*(1 -+ 2^-20) differ, which brackets
+  //      the exact FP64 quotient; flagged elements are re-encoded from it.  Codes go to a transposed
+  //      smem tile: RT-byte unit (channel c, keys [rg*RT, +RT)) at unit index rg ^ swz(c8).
+  {
+    const float lo_f = 1.0f - 0x1p-20f, hi_f = 1.0f + 0x1p-20f;
+    const int swz = c8 * (UPR / LPR);
+    uint32_t tmask = 0u;  // bit i*RT + rr: element (channel c0+i, key rg*RT+rr) is near a tie
 #pragma unroll
-      for (int c = 0; c < D / 4; ++c) {
-        const int cc = qq * (D / 4) + c;
-        a4[c & 3] = fma(qmu[cc], static_cast<double>(to_f32<T>(kraw[r * D + cc])) - kmu[cc], a4[c & 3]);
+    for (int i = 0; i < 8; ++i) {
+      const int c = c0 + i;
+      const float inv = s_vinv[c];
+      uint32_t unit = 0u;
+#pragma unroll
+      for (int rr = 0; rr < RT; rr += 2) {
+        const float2 q = __fmul2_rn(make_float2(vt[rr].get(i), vt[rr + 1].get(i)), make_float2(inv, inv));
+        const float2 ql = __fmul2_rn(q, make_float2(lo_f, lo_f));
+        const float2 qh = __fmul2_rn(q, make_float2(hi_f, hi_f));
+        uint16_t cq, cl, ch;
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(cq) : "f"(q.y), "f"(q.x));
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(cl) : "f"(ql.y), "f"(ql.x));
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(ch) : "f"(qh.y), "f"(qh.x));
+        const uint32_t d = static_cast<uint32_t>(cl ^ ch);
+        tmask |= (((d & 0xFFu) != 0u ? 1u : 0u) | ((d >> 8) != 0u ? 2u : 0u)) << (i * RT + rr);
+        unit |= static_cast<uint32_t>(cq) << (8 * rr);
       }
-      acc = (a4[0] + a4[1]) + (a4[2] + a4[3]);
+      uint8_t* dst = s_vt + c * 64 + ((rg ^ swz) * RT);
+      if constexpr (RT == 4) {
+        *reinterpret_cast<uint32_t*>(dst) = unit;
+      } else {
+        *reinterpret_cast<uint16_t*>(dst) = static_cast<uint16_t>(unit);
+      }
     }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (qq == 0) {
-      const int64_t o = (static_cast<int64_t>(b) * Hq + hq) * Np + n0 + r;
-      bias[o] = static_cast<float>(acc);
-      bias_l2[o] = static_cast<float>(acc * sm_scale_log2);
+    // ~0.6% of bf16 elements sit exactly on an E4M3 tie: re-encode just those from the FP64
+    // quotient (a warp loops max-popcount times, ~1-2)
+    while (tmask) {
+      const int bit = __ffs(tmask) - 1;
+      tmask &= tmask - 1u;
+      const int i = bit / RT, rr = bit % RT, c = c0 + i;
+      const float x = to_f32<T>(row_ptr<T>(v_in, b, h, n0 + rg * RT + rr)[c]);
+      s_vt[c * 64 + (rg ^ swz) * RT + rr] = v_code_exact(x, s_vsc[c]);
     }
+  }
+
+  // ---- bias for every query head sharing this KV head: b_j = q_mean . Ks_j (attention.py:288-289),
+  //      FP64 over this thread's 8 channels, then a butterfly over the LPR lanes of the row
+  {
+    const int group = Hq / Hkv;
+    double km[8];
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      const double2 m2 = *reinterpret_cast<const double2*>(kmu_g + c0 + i);
+      km[i] = m2.x;
+      km[i + 1] = m2.y;
+    }
+    for (int g = 0; g < group; ++g) {
+      const int hq = h * group + g;
+      double acc[RT];
+#pragma unroll
+      for (int rr = 0; rr < RT; ++rr) acc[rr] = 0.0;
+      if (smoothing) {
+        const double* qm_g = means + (static_cast<int64_t>(b) * Ht + hq) * D + c0;
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          const double2 q2 = *reinterpret_cast<const double2*>(qm_g + i);
+#pragma unroll
+          for (int rr = 0; rr < RT; ++rr) {
+            acc[rr] = fma(q2.x, static_cast<double>(kt[rr].get(i)) - km[i], acc[rr]);
+            acc[rr] = fma(q2.y, static_cast<double>(kt[rr].get(i + 1)) - km[i + 1], acc[rr]);
+          }
+        }
+#pragma unroll
+        for (int o = 1; o < LPR; o <<= 1) {
+#pragma unroll
+          for (int rr = 0; rr < RT; ++rr) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
+        }
+      }
+      if (c8 < RT) {
+        const int r = rg * RT + c8;
+        double a = acc[0];
+#pragma unroll
+        for (int rr = 1; rr < RT; ++rr)
+          if (c8 == rr) a = acc[rr];
+        if (r >= rows) a = 0.0;
+        const int64_t o = (static_cast<int64_t>(b) * Hq + hq) * Np + n0 + r;
+        bias[o] = static_cast<float>(a);
+        bias_l2[o] = static_cast<float>(a * sm_scale_log2);
+      }
+    }
+  }
+
+  // ---- V^T codes out: lane -> (channel, 4-key word); two channels per warp instruction, 64 B each
+  __syncthreads();
+  constexpr int WSWZ = (UPR / LPR) * RT / 4;  // the unit swizzle in 4-byte words
+#pragma unroll
+  for (int it = 0; it < D / 16; ++it) {
+    const int idx = it * 256 + tid;
+    const int c = idx >> 4, j = idx & 15;
+    const uint32_t v = *reinterpret_cast<const uint32_t*>(s_vt + c * 64 + 4 * (j ^ ((c >> 3) * WSWZ)));
+    *reinterpret_cast<uint32_t*>(v_codes + (static_cast<int64_t>(bh) * D + c) * Np + n0 + 4 * j) = v;
   }
 }
 
