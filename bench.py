@@ -322,7 +322,7 @@ def run_ours(a):
         hq, hk, hv = (t.cpu().pin_memory() for t in src)
         ho = torch.empty(src[0].shape, dtype=out.dtype, pin_memory=True)
         pipe = None if ulysses else sa.HostPipeline(1, Ul, Ul // group, N, D, torch.bfloat16, dev,
-                                                    is_causal=a.causal, pv_accum=a.pv_accum, chunks=16)
+                                                    is_causal=a.causal, pv_accum=a.pv_accum)
 
         def e2e_step():
             if ulysses:

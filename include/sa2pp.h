@@ -6,8 +6,8 @@
  * and for the north-star API  sageattn(q, k, v, tensor_layout, is_causal, sm_scale).
  *
  * Plain C: device pointers, sizes, element strides, a caller-owned CUDA stream.
- * No torch or C++ types cross this boundary, no exceptions, no allocation, no
- * host synchronisation.  Every entry point returns an sa2pp_status; the text of
+ * No torch or C++ types cross this boundary, no exceptions, no allocation (except
+ * the host-pipeline handle, which owns its buffers and streams), no host synchronisation.  Every entry point returns an sa2pp_status; the text of
  * the last failure on the calling thread is available from sa2pp_last_error().
  *
  * Mapping onto the reference (file:line of the code each entry point replaces):
@@ -18,6 +18,8 @@
  *                   FP8 PV with FP16 (or FP32) accumulation, promotion, 1/l
  *                   (attention.py:279-305; mma.py:116-181)
  *   sa2pp_sageattn  both of the above: attention_quantized (attention.py:232)
+ *   sa2pp_host_pipeline_*  the same operator on host arrays, PCIe overlapped
+ *                   (attention_quantized's numpy-in / numpy-out contract)
  *   sa2pp_problem   AttentionConfig + RangeConfig (attention.py:58-95,
  *                   quantization.py:33-68)
  */
@@ -148,6 +150,24 @@ SA2PP_API int sa2pp_attn_fwd(const sa2pp_problem* prob, const sa2pp_quant* qt, c
 /* Prepass + attention in one call: the attention_quantized / sageattn operator. */
 SA2PP_API int sa2pp_sageattn(const sa2pp_problem* prob, const sa2pp_inputs* in, const sa2pp_quant* qt, void* workspace,
                    size_t workspace_bytes, const sa2pp_output* out, sa2pp_report* report, void* cuda_stream);
+
+/* Host-memory operator (reference: attention_quantized takes and returns host arrays,
+ * attention.py:232-316).  Q [B,Hq,N,D], K and V [B,Hkv,N,D], O [B,Hq,N,D], contiguous HND host
+ * memory in `dtype` (pinned memory for full PCIe overlap; pageable works, serialised).
+ * The (batch, kv-head) units are cut into `chunks` and pipelined through `depth` device buffer
+ * sets: upload, sa2pp_sageattn and download of successive chunks overlap on three internal
+ * streams, and the ring carries over between calls so back-to-back calls overlap as well.
+ * This is the one entry point that owns device memory and streams (allocated at create).
+ *
+ * run() only enqueues.  The host inputs must be ready when it is called and stay unmodified,
+ * and O is complete, once `cuda_stream` (made to wait for the last download) reaches the point
+ * after the call.  The uploads do not wait for earlier work on `cuda_stream`. */
+typedef struct sa2pp_host_pipeline sa2pp_host_pipeline;
+SA2PP_API int sa2pp_host_pipeline_create(const sa2pp_problem* prob, int dtype, int chunks, int depth,
+                                         sa2pp_host_pipeline** out);
+SA2PP_API int sa2pp_host_pipeline_run(sa2pp_host_pipeline* hp, const void* q, const void* k, const void* v, void* o,
+                                      void* cuda_stream);
+SA2PP_API int sa2pp_host_pipeline_destroy(sa2pp_host_pipeline* hp);
 
 /* Debug/introspection: dump raw TMEM of the first block of CTA 0 (S int32 [128,64] and
  * the promoted-before-scaling PV words [128,D]) into `dbg` (device, >= 128*(64+D)*4 bytes).

@@ -19,7 +19,8 @@ SA2PP_ACC_F16, SA2PP_ACC_F32 = range(2)
 EXPORTED = (
     "sa2pp_version", "sa2pp_last_error", "sa2pp_check_problem", "sa2pp_quant_sizes",
     "sa2pp_prepass", "sa2pp_attn_fwd", "sa2pp_sageattn", "sa2pp_set_debug_buffer",
-    "sa2pp_set_trace_buffer",
+    "sa2pp_set_trace_buffer", "sa2pp_host_pipeline_create", "sa2pp_host_pipeline_run",
+    "sa2pp_host_pipeline_destroy",
 )
 
 
@@ -84,6 +85,9 @@ def lib() -> C.CDLL:
                                      P(Output), C.c_void_p, C.c_void_p]
         h.sa2pp_set_debug_buffer.argtypes = [C.c_void_p]
         h.sa2pp_set_trace_buffer.argtypes = [C.c_void_p]
+        h.sa2pp_host_pipeline_create.argtypes = [P(Problem), C.c_int, C.c_int, C.c_int, P(C.c_void_p)]
+        h.sa2pp_host_pipeline_run.argtypes = [C.c_void_p] * 6
+        h.sa2pp_host_pipeline_destroy.argtypes = [C.c_void_p]
         for name in EXPORTED[2:]:
             getattr(h, name).restype = C.c_int
         _lib = h

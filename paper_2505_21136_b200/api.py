@@ -152,75 +152,59 @@ def sageattn(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, tensor_layout: s
 class HostPipeline:
     """`sageattn` on pinned HOST tensors with the copies overlapped with the kernels.
 
-    The (batch, kv-head) units are cut into `chunks` (whole GQA groups, so every chunk is an
+    A thin owner of the native handle `sa2pp_host_pipeline_*` (csrc/host_pipeline.cu): the
+    (batch, kv-head) units are cut into `chunks` (whole GQA groups, so every chunk is an
     independent attention problem: smoothing statistics are per head); chunk i's host->device
-    copy, prepass + attention and device->host copy run on three streams through a ring of
-    `depth` device buffer sets, so PCIe traffic in both directions overlaps the tensor cores.
-    Inputs [B, H, N, D] (HND, contiguous, pinned); the output is written into `out` (pinned).
-    The caller's current stream is ordered after the last copy-back.
+    copy, prepass + attention and device->host copy run on three native streams through a ring
+    of `depth` device buffer sets that persists across calls, so PCIe traffic in both
+    directions overlaps the tensor cores and consecutive calls overlap each other.
+    Inputs [B, H, N, D] (HND, contiguous, pinned); the output is written into `out` (pinned) and
+    is complete once the caller's current stream reaches the point after the call.  Inputs must
+    be ready when called (the uploads do not wait for earlier work on the caller's stream).
     """
 
     def __init__(self, B, Hq, Hkv, N, D, dtype=torch.bfloat16, device="cuda", *, is_causal=False,
-                 sm_scale=None, pv_accum="fp16", chunks=8, depth=2, **kw):
+                 sm_scale=None, pv_accum="fp16", chunks=16, depth=3, **kw):
         if Hq % Hkv:
             raise ValueError("heads_q must be a multiple of heads_kv")
-        self.B, self.Hq, self.Hkv, self.N, self.D = B, Hq, Hkv, N, D
-        self.group = Hq // Hkv
+        if dtype not in _DT:
+            raise ValueError("dtype must be float16, bfloat16 or float32")
+        self.B, self.Hq, self.Hkv, self.N, self.D, self.dtype = B, Hq, Hkv, N, D, dtype
         self.device = torch.device(device)
-        self.causal, self.sm_scale, self.pv_accum, self.kw = is_causal, sm_scale, pv_accum, kw
-        units = B * Hkv
-        self.cu = -(-units // max(1, min(chunks, units)))  # kv units per chunk
-        self.spans = [(u, min(units, u + self.cu)) for u in range(0, units, self.cu)]
-        self.depth = max(1, min(depth, len(self.spans)))
-        g, cu = self.group, self.cu
-        mk = lambda h: torch.empty(1, h, N, D, dtype=dtype, device=self.device)  # noqa: E731
-        self.bufs = [(mk(cu * g), mk(cu), mk(cu), mk(cu * g)) for _ in range(self.depth)]
-        prob = _problem(1, cu * g, cu, N, D, causal=is_causal, pv_accum=pv_accum, sm_scale=sm_scale,
+        if self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
+        prob = _problem(B, Hq, Hkv, N, D, causal=is_causal, pv_accum=pv_accum, sm_scale=sm_scale,
                         smoothing=kw.get("smooth", True), qk_bits=kw.get("qk_bits", 8),
                         p_r=kw.get("p_r", 224.0), v_r=kw.get("v_r", 4.5))
-        self.quant = [alloc_quant(prob, self.device) for _ in range(self.depth)]
-        self.h2d, self.comp, self.d2h = (torch.cuda.Stream(self.device) for _ in range(3))
-        ev = lambda: [torch.cuda.Event() for _ in range(self.depth)]  # noqa: E731
-        self.ev_in, self.ev_comp, self.ev_out = ev(), ev(), ev()
+        self._h = A.C.c_void_p()
+        with torch.cuda.device(self.device):
+            A.check(A.lib().sa2pp_host_pipeline_create(C_ref(prob), _DT[dtype], chunks, depth, A.C.byref(self._h)))
 
     def __call__(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor) -> torch.Tensor:
-        B, Hq, Hkv, N, D, g = self.B, self.Hq, self.Hkv, self.N, self.D, self.group
+        B, Hq, Hkv, N, D = self.B, self.Hq, self.Hkv, self.N, self.D
         for t, h in ((q, Hq), (k, Hkv), (v, Hkv), (out, Hq)):
-            if t.is_cuda or tuple(t.shape) != (B, h, N, D) or not t.is_contiguous():
-                raise ValueError("HostPipeline takes contiguous [B, H, N, D] host tensors")
-        qf, kf, vf, of = (t.view(-1, N, D) for t in (q, k, v, out))
+            if t.is_cuda or tuple(t.shape) != (B, h, N, D) or not t.is_contiguous() or t.dtype != self.dtype:
+                raise ValueError("HostPipeline takes contiguous [B, H, N, D] host tensors of its dtype")
         caller = torch.cuda.current_stream(self.device)
-        self.h2d.wait_stream(caller)
-        for i, (u0, u1) in enumerate(self.spans):
-            s = i % self.depth
-            dq, dk, dv, do = self.bufs[s]
-            n = u1 - u0
-            with torch.cuda.stream(self.h2d):
-                if i >= self.depth:
-                    self.h2d.wait_event(self.ev_out[s])  # buffer set s copied back
-                dq[0, :n * g].copy_(qf[u0 * g:u1 * g], non_blocking=True)
-                dk[0, :n].copy_(kf[u0:u1], non_blocking=True)
-                dv[0, :n].copy_(vf[u0:u1], non_blocking=True)
-                self.ev_in[s].record(self.h2d)
-            with torch.cuda.stream(self.comp):
-                self.comp.wait_event(self.ev_in[s])
-                if n == self.cu:
-                    sageattn(dq, dk, dv, "HND", self.causal, self.sm_scale, pv_accum=self.pv_accum, out=do,
-                             quant=self.quant[s], stream=self.comp, **self.kw)
-                else:  # ragged last chunk
-                    sageattn(dq[:, :n * g], dk[:, :n], dv[:, :n], "HND", self.causal, self.sm_scale,
-                             pv_accum=self.pv_accum, out=do[:, :n * g], stream=self.comp, **self.kw)
-                self.ev_comp[s].record(self.comp)
-            with torch.cuda.stream(self.d2h):
-                self.d2h.wait_event(self.ev_comp[s])
-                of[u0 * g:u1 * g].copy_(do[0, :n * g], non_blocking=True)
-                self.ev_out[s].record(self.d2h)
-        caller.wait_stream(self.d2h)
+        with torch.cuda.device(self.device):
+            A.check(A.lib().sa2pp_host_pipeline_run(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                                    out.data_ptr(), caller.cuda_stream))
         return out
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) and self._h.value:
+            A.lib().sa2pp_host_pipeline_destroy(self._h)
+            self._h = A.C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def sageattn_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, is_causal: bool = False,
-                  sm_scale: Optional[float] = None, *, out: Optional[torch.Tensor] = None, chunks: int = 8,
+                  sm_scale: Optional[float] = None, *, out: Optional[torch.Tensor] = None, chunks: int = 16,
                   **kw) -> torch.Tensor:
     """One-shot `HostPipeline` call: pinned HND host tensors in, pinned host output out."""
     B, Hq, N, D = q.shape

@@ -391,7 +391,7 @@ __host__ __device__ constexpr int kv_smem_bytes() {
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InView v_in, int Hq, int Hkv, int N, int Np,
+__global__ void __launch_bounds__(256, 3) quantize_kv_kernel(InView kv_in, InView v_in, int Hq, int Hkv, int N, int Np,
                                                              int n_kb, int qmax, double v_r, int smoothing,
                                                              double sm_scale_log2, const double* __restrict__ means,
                                                              int Ht, int8_t* __restrict__ k_codes,

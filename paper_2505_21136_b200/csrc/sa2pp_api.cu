@@ -16,14 +16,19 @@ thread_local std::string g_last_error;
 uint32_t* g_debug = nullptr;
 unsigned long long* g_trace = nullptr;
 
-int fail(int code, const char* fmt, ...) {
+int vfail(int code, const char* fmt, va_list ap) {
   char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
   vsnprintf(buf, sizeof(buf), fmt, ap);
-  va_end(ap);
   g_last_error = buf;
   return code;
+}
+
+int fail(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  const int rc = vfail(code, fmt, ap);
+  va_end(ap);
+  return rc;
 }
 
 int cuda_fail(cudaError_t e, const char* where) {
@@ -54,6 +59,14 @@ double sm_scale_of(const sa2pp_problem& p) {
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
 
 }  // namespace
+
+int sa2pp::set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  const int rc = vfail(code, fmt, ap);
+  va_end(ap);
+  return rc;
+}
 
 extern "C" {
 

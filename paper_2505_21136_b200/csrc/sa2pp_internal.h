@@ -10,6 +10,9 @@ namespace sa2pp {
 constexpr int kBlockQ = 128;  // attention.py:62
 constexpr int kBlockK = 64;   // attention.py:63
 
+// Record the calling thread's last error (sa2pp_last_error) and return `code`.
+int set_error(int code, const char* fmt, ...);
+
 struct PrepassLaunch {
   int dtype, D, B, Hq, Hkv, N, Nq_pad, Np, n_qt, n_kb, qmax, smoothing;
   int rows_per_chunk, n_chunks;

@@ -121,3 +121,18 @@ def test_reference_mirror_rejects_like_reference():
         sa.attention_quantized(z, z, z, sa.AttentionConfig(seq_len=64, head_dim=48))
     with pytest.raises(ValueError):
         sa.attention_quantized(z, z, z[:, :32], sa.AttentionConfig(seq_len=64, head_dim=48))
+
+
+def test_host_pipeline_validates_before_touching_the_gpu():
+    """sa2pp_host_pipeline_create rejects bad problems/knobs with the reference's error classes
+    before any CUDA call; run/destroy accept only real handles."""
+    lib = A.lib()
+    h = ctypes.c_void_p()
+    prob = _problem(1, 4, 3, 128, 64, causal=False)  # heads_q % heads_kv != 0
+    assert lib.sa2pp_host_pipeline_create(ctypes.byref(prob), A.SA2PP_BF16, 4, 2, ctypes.byref(h)) == A.SA2PP_ERR_INVALID
+    prob = _problem(1, 4, 4, 128, 64, causal=False)
+    assert lib.sa2pp_host_pipeline_create(ctypes.byref(prob), 7, 4, 2, ctypes.byref(h)) == A.SA2PP_ERR_INVALID
+    assert lib.sa2pp_host_pipeline_create(ctypes.byref(prob), A.SA2PP_BF16, 0, 2, ctypes.byref(h)) == A.SA2PP_ERR_INVALID
+    assert h.value is None
+    assert lib.sa2pp_host_pipeline_run(None, None, None, None, None, None) == A.SA2PP_ERR_INVALID
+    assert lib.sa2pp_host_pipeline_destroy(None) == A.SA2PP_OK
