@@ -160,18 +160,6 @@ __global__ void channel_means_kernel(const double2* __restrict__ partial, int n_
 }
 
 // ------------------------------------------------------------------ shared helpers
-__device__ __forceinline__ double block_max_256(double x, double* scratch) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
-  const int w = threadIdx.x >> 5;
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) scratch[w] = x;
-  __syncthreads();
-  double m = scratch[0];
-#pragma unroll
-  for (int i = 1; i < 8; ++i) m = fmax(m, scratch[i]);
-  return m;
-}
 
 // Direct FP64 -> E4M3 ("fn") with RNE and saturation to +-448 (numerics.py:152-182).
 __device__ __forceinline__ uint8_t e4m3_from_f64(double x) {
@@ -217,138 +205,17 @@ __device__ __forceinline__ uint8_t e4m3_div(double x, double scale, double inv) 
   return e4m3_from_f64(q);
 }
 
-
-
-// Branch-free halves of the fast paths: the code assuming no tie, and whether the element is near
-// one.  Callers OR the flags over a batch and redo the whole batch exactly in the rare case, so the
-// common path carries no per-element divergence/reconvergence.
-__device__ __forceinline__ int int_code_nt(float v, float mu_hi, float mu_lo, float inv32, int qmax, bool& tie) {
-  const float q = ((v - mu_hi) - mu_lo) * inv32;
-  const float t = q + 12582912.0f;  // 1.5 * 2^23
-  tie |= fabsf(fabsf(q - (t - 12582912.0f)) - 0.5f) < 1e-4f;
-  return min(max(__float_as_int(t) - 0x4B400000, -qmax), qmax);
-}
+// The exact integer code: the FP64 quotient of the smoothed value (quantization.py:151-160).
 __device__ __forceinline__ int int_code_exact(float v, double mu, double scale, double inv64, int qmax) {
   return min(max(static_cast<int>(div_rint(static_cast<double>(v) - mu, scale, inv64)), -qmax), qmax);
 }
-__device__ __forceinline__ uint32_t e4m3_nt(float v, float inv32, bool& tie) {
-  const float q = v * inv32;
-  const uint32_t a = __float_as_uint(q) & 0x7FFFFFFFu;
-  const uint32_t d = a & 0xFFFFFu;
-  const float y = __uint_as_float(a) * 512.0f;
-  tie |= a >= 0x3C800000u ? (d > 0x80000u - 64u && d < 0x80000u + 64u) : (fabsf((y - truncf(y)) - 0.5f) < 1e-4f);
-  uint16_t r;
-  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(0.0f), "f"(q));
-  return r & 0xFFu;
-}
 
-// ------------------------------------------------------------------ pass 2: Q tiles
-// One CTA (256 threads) per 128-row tile of one (b, hq).  Rows >= N are written as zero codes.
-// amax = max over channels of max(|max_c - mu_c|, |min_c - mu_c|): fl64(v - mu) is monotone in v, so
-// this is the reference's max |fl64(v - mu)| over the tile with FP64 work per channel only.
-template <typename T, int D>
-__global__ void __launch_bounds__(256) quantize_q_kernel(InView qv, int Hq, int N, int Nq_pad, int n_qt, int qmax,
-                                                         const double* __restrict__ means, int Ht,
-                                                         int8_t* __restrict__ q_codes, float* __restrict__ q_scale,
-                                                         double* __restrict__ q_scale64) {
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int LANES_PER_ROW = D / VEC;
-  constexpr int ROWS_PER_PASS = 256 / LANES_PER_ROW;
-  __shared__ double scratch[8];
-  const int qt = blockIdx.x;
-  const int bh = blockIdx.y;
-  const int b = bh / Hq, h = bh % Hq;
-  const int c8 = threadIdx.x % LANES_PER_ROW;
-  const int r0 = threadIdx.x / LANES_PER_ROW;
-  const int n0 = qt * 128;
-  const int n1 = min(N, n0 + 128);
-  float mn[VEC], mx[VEC];
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) {
-    mn[i] = INFINITY;
-    mx[i] = -INFINITY;
-  }
-  for (int n = n0 + r0; n < n1; n += ROWS_PER_PASS) {
-    const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(qv, b, h, n) + c8 * VEC);
-    const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      const float x = to_f32<T>(e[i]);
-      mn[i] = fminf(mn[i], x);
-      mx[i] = fmaxf(mx[i], x);
-    }
-  }
-  const double* mup = means + (static_cast<int64_t>(b) * Ht + h) * D + c8 * VEC;
-  double amax = 0.0, mumax = 0.0;
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) {
-    const double m = mup[i];
-    if (mx[i] >= mn[i])
-      amax = fmax(amax, fmax(fabs(static_cast<double>(mx[i]) - m), fabs(static_cast<double>(mn[i]) - m)));
-    mumax = fmax(mumax, fabs(m));
-  }
-  amax = block_max_256(amax, scratch);
-  mumax = block_max_256(mumax, scratch);
-  const double scale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
-  if (threadIdx.x == 0) {
-    q_scale[static_cast<int64_t>(bh) * n_qt + qt] = static_cast<float>(scale);
-    q_scale64[static_cast<int64_t>(bh) * n_qt + qt] = scale;
-  }
-  const double inv = 1.0 / scale;
-  const float inv32 = static_cast<float>(inv);
-  const bool fast = mumax <= 65536.0 * amax;  // the error bound of int_code_nt
-  float mu_hi[VEC], mu_lo[VEC];
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) {
-    mu_hi[i] = static_cast<float>(mup[i]);
-    mu_lo[i] = static_cast<float>(mup[i] - static_cast<double>(mu_hi[i]));
-  }
-  int8_t* dst = q_codes + (static_cast<int64_t>(bh) * Nq_pad) * D;
-  for (int n = n0 + r0; n < n0 + 128; n += ROWS_PER_PASS) {
-    uint32_t w[VEC / 4];
-#pragma unroll
-    for (int i = 0; i < VEC / 4; ++i) w[i] = 0u;
-    if (n < n1) {
-      const uint4 raw = *reinterpret_cast<const uint4*>(row_ptr<T>(qv, b, h, n) + c8 * VEC);
-      const T* e = reinterpret_cast<const T*>(&raw);
-      uint32_t tmask = fast ? 0u : (1u << VEC) - 1u;
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        bool tie = false;
-        w[i >> 2] |= (static_cast<uint32_t>(int_code_nt(to_f32<T>(e[i]), mu_hi[i], mu_lo[i], inv32, qmax, tie)) & 0xFFu)
-                     << (8 * (i & 3));
-        tmask |= static_cast<uint32_t>(tie) << i;
-      }
-      while (tmask) {  // rare: near a rounding tie or |mu| >> amax -> the FP64 quotient per element
-        const int i = __ffs(tmask) - 1;
-        tmask &= tmask - 1u;
-        const float x = to_f32<T>(row_ptr<T>(qv, b, h, n)[c8 * VEC + i]);
-        const uint32_t code = static_cast<uint32_t>(int_code_exact(x, mup[i], scale, inv, qmax)) & 0xFFu;
-        const int sh = 8 * (i & 3);
-#pragma unroll
-        for (int k = 0; k < VEC / 4; ++k)
-          if (k == (i >> 2)) w[k] = (w[k] & ~(0xFFu << sh)) | (code << sh);
-      }
-    }
-    int8_t* o = dst + static_cast<int64_t>(n) * D + c8 * VEC;
-    if constexpr (VEC == 8) {
-      *reinterpret_cast<uint2*>(o) = make_uint2(w[0], w[1]);
-    } else {
-      *reinterpret_cast<uint32_t*>(o) = w[0];
-    }
-  }
-}
+// Integer-code tie window of the FP32 fast path.  Under the fast-path condition |mu| <= 65536*amax,
+// |q_fp32 - q_fp64| <= 2^-22 * qmax (two f32 roundings of d = (v - mu_hi) - mu_lo relative to amax, the
+// f32 reciprocal and the product), i.e. 3.03e-5 at qmax = 127; codes whose fractional part lies within
+// 4e-5 of .5 are recomputed from the FP64 quotient.
+constexpr float kTieEdge = 0.5f - 4e-5f;
 
-// ------------------------------------------------------------------ pass 3: K/V blocks
-// One CTA (256 threads) per 64-key block of one (b, hkv).  Thread (rg, c8) holds channels
-// [8*c8, 8*c8+8) of the RT consecutive keys [rg*RT, rg*RT+RT) of both K and V in registers, so the
-// block is read from HBM exactly once and every output is produced from registers:
-//   k_codes  [B, Hkv, Np, D]          int8, 8-byte stores straight from registers
-//   v_codes  [B, Hkv, D, Np]          E4M3, transposed through a swizzled 64-byte-per-channel smem tile
-//   kv_meta  [B, Hkv, nKB, 4 + D]     f32 {dK, 0, 0, 0, dV[0..D)}
-//   bias     [B, Hq, Np]              f32 q_mean . Ks_j ; bias_l2 = bias * sm_scale * log2(e)
-// Per-channel statistics (K min/max, V |max|) are reduced across the row groups with shuffles and
-// across warps through shared memory; the block scalars need two CTA barriers, the transpose a third.
 // Rare-path encoders kept out of line so the unrolled fast paths stay small in the i-cache.
 __device__ __noinline__ uint32_t k_codes_exact8(const float* x, const double* mu, double scale, double inv, int qmax,
                                                  uint32_t* w1) {
@@ -385,13 +252,220 @@ struct KvTile {
   __device__ __forceinline__ float2 get2(int i) const { return make_float2(get(i), get(i + 1)); }
 };
 
+// ------------------------------------------------------------------ pass 2: Q tiles
+// Persistent CTAs (256 threads) walk the 128-row tiles of all (b, hq).  Thread (rg, c8) owns channels
+// [8*c8, 8*c8+8) of the RT consecutive rows [rg*RT, rg*RT+RT): it cp.asyncs exactly those bytes of
+// the NEXT tile into its own shared-memory slots while it quantizes the current one from registers,
+// so every CTA keeps a tile in flight (the kernel is HBM-latency-bound otherwise) and no barrier is
+// needed for the staging.  Rows >= N are written as zero codes.  amax = max over channels of
+// max(|max_c - mu_c|, |min_c - mu_c|): fl64(v - mu) is monotone in v, so this is the reference's
+// max |fl64(v - mu)| over the tile (quantization.py:151-160) with FP64 work per channel only.
+template <typename T, int D>
+__host__ __device__ constexpr int q_smem_bytes() {
+  return 2 * 128 * D * static_cast<int>(sizeof(T));
+}
+
+template <typename T>
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc, bool valid) {
+  const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(gsrc), "r"(valid ? 16 : 0) : "memory");
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256, 2) quantize_q_kernel(InView qv, int Hq, int N, int Nq_pad, int n_qt, int n_tiles, int qmax,
+                                                            const double* __restrict__ means, int Ht,
+                                                            int8_t* __restrict__ q_codes, float* __restrict__ q_scale,
+                                                            double* __restrict__ q_scale64) {
+  constexpr int LPR = D / 8;      // lanes per row
+  constexpr int RPP = 256 / LPR;  // row groups per CTA
+  constexpr int RT = 128 / RPP;   // consecutive rows per thread (8 for D=128, 4 for D=64)
+  constexpr int NW = sizeof(T) == 4 ? 2 : 1;  // 16-byte pieces per 8 channels
+  constexpr int SLOT = RT * NW;               // 16-byte pieces per thread per tile
+  extern __shared__ __align__(16) unsigned char q_smem[];
+  uint4* stage = reinterpret_cast<uint4*>(q_smem);  // [2][SLOT][256]
+  __shared__ float s_mn[8 * D], s_mx[8 * D];
+  __shared__ double s_red[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c8 = tid % LPR, rg = tid / LPR;
+  const int c0 = c8 * 8;
+  auto prefetch = [&](int tile, int slot) {
+    const int qt = tile % n_qt, bh = tile / n_qt;
+    const int b = bh / Hq, h = bh % Hq;
+    const int n0 = qt * 128;
+#pragma unroll
+    for (int rr = 0; rr < RT; ++rr) {
+      const int r = n0 + rg * RT + rr;
+      const T* src = row_ptr<T>(qv, b, h, r < N ? r : 0) + c0;
+#pragma unroll
+      for (int u = 0; u < NW; ++u)
+        cp_async16<T>(&stage[(slot * SLOT + rr * NW + u) * 256 + tid], reinterpret_cast<const uint4*>(src) + u, r < N);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int slot = 0;
+  if (static_cast<int>(blockIdx.x) < n_tiles) prefetch(blockIdx.x, 0);
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, slot ^= 1) {
+    const int qt = tile % n_qt, bh = tile / n_qt;
+    const int b = bh / Hq, h = bh % Hq;
+    const int n0 = qt * 128;
+    const int rows = min(128, N - n0);
+    const double* mu_g = means + (static_cast<int64_t>(b) * Ht + h) * D;
+    const int next = tile + gridDim.x;
+    if (next < n_tiles) {
+      prefetch(next, slot ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    KvTile<T> x[RT];
+#pragma unroll
+    for (int rr = 0; rr < RT; ++rr)
+#pragma unroll
+      for (int u = 0; u < NW; ++u) {
+        const uint4 v4 = stage[(slot * SLOT + rr * NW + u) * 256 + tid];
+        x[rr].w[4 * u] = v4.x; x[rr].w[4 * u + 1] = v4.y; x[rr].w[4 * u + 2] = v4.z; x[rr].w[4 * u + 3] = v4.w;
+      }
+    const double mu_c = tid < D ? mu_g[tid] : 0.0;
+    float2 mh[4], ml[4];
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      const double2 m2 = *reinterpret_cast<const double2*>(mu_g + c0 + i);
+      mh[i / 2] = make_float2(static_cast<float>(m2.x), static_cast<float>(m2.y));
+      ml[i / 2] = make_float2(static_cast<float>(m2.x - static_cast<double>(mh[i / 2].x)),
+                              static_cast<float>(m2.y - static_cast<double>(mh[i / 2].y)));
+    }
+
+    {  // per-channel min/max over the tile's valid rows
+      float mn[8], mx[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        mn[i] = INFINITY;
+        mx[i] = -INFINITY;
+      }
+      if (rows == 128) {
+#pragma unroll
+        for (int rr = 0; rr < RT; ++rr)
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            mn[i] = fminf(mn[i], x[rr].get(i));
+            mx[i] = fmaxf(mx[i], x[rr].get(i));
+          }
+      } else {
+#pragma unroll
+        for (int rr = 0; rr < RT; ++rr) {
+          const bool ok = rg * RT + rr < rows;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            mn[i] = fminf(mn[i], ok ? x[rr].get(i) : INFINITY);
+            mx[i] = fmaxf(mx[i], ok ? x[rr].get(i) : -INFINITY);
+          }
+        }
+      }
+#pragma unroll
+      for (int o = LPR; o < 32; o <<= 1)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          mn[i] = fminf(mn[i], __shfl_xor_sync(0xffffffffu, mn[i], o));
+          mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
+        }
+      if (lane < LPR) {
+        float* d0 = s_mn + warp * D + c0;
+        float* d1 = s_mx + warp * D + c0;
+        *reinterpret_cast<float4*>(d0) = make_float4(mn[0], mn[1], mn[2], mn[3]);
+        *reinterpret_cast<float4*>(d0 + 4) = make_float4(mn[4], mn[5], mn[6], mn[7]);
+        *reinterpret_cast<float4*>(d1) = make_float4(mx[0], mx[1], mx[2], mx[3]);
+        *reinterpret_cast<float4*>(d1 + 4) = make_float4(mx[4], mx[5], mx[6], mx[7]);
+      }
+    }
+    __syncthreads();
+    if (tid < D) {
+      float mn = INFINITY, mx = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        mn = fminf(mn, s_mn[w * D + tid]);
+        mx = fmaxf(mx, s_mx[w * D + tid]);
+      }
+      double amax = 0.0;
+      if (mx >= mn) amax = fmax(fabs(static_cast<double>(mx) - mu_c), fabs(static_cast<double>(mn) - mu_c));
+      double mumax = fabs(mu_c);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        mumax = fmax(mumax, __shfl_xor_sync(0xffffffffu, mumax, o));
+      }
+      if (lane == 0) {
+        s_red[warp] = amax;
+        s_red[4 + warp] = mumax;
+      }
+    }
+    __syncthreads();
+    double amax = s_red[0], mumax = s_red[4];
+#pragma unroll
+    for (int w = 1; w < D / 32; ++w) {
+      amax = fmax(amax, s_red[w]);
+      mumax = fmax(mumax, s_red[4 + w]);
+    }
+    const double scale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
+    if (tid == 0) {
+      q_scale[static_cast<int64_t>(bh) * n_qt + qt] = static_cast<float>(scale);
+      q_scale64[static_cast<int64_t>(bh) * n_qt + qt] = scale;
+    }
+    const double inv = 1.0 / scale;
+    const float inv32 = static_cast<float>(inv);
+    const bool fast = mumax <= 65536.0 * amax;  // the error bound of the FP32 fast path
+
+    // codes: ((q - mu_hi) - mu_lo) * inv rounded with the 1.5*2^23 trick; the code is the low byte
+    // of the rounded float's bits (|q| <= qmax + 3e-5 under `fast`, so no clamp is needed)
+    const float2 inv2 = make_float2(inv32, inv32);
+    const float2 magic2 = make_float2(12582912.0f, 12582912.0f);
+    int8_t* dst = q_codes + (static_cast<int64_t>(bh) * Nq_pad + n0 + rg * RT) * D + c0;
+#pragma unroll
+    for (int rr = 0; rr < RT; ++rr) {
+      uint32_t tb[8];
+      bool tie = !fast;
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const float2 d = __fadd2_rn(__fadd2_rn(x[rr].get2(i), make_float2(-mh[i / 2].x, -mh[i / 2].y)),
+                                    make_float2(-ml[i / 2].x, -ml[i / 2].y));
+        const float2 t = __ffma2_rn(d, inv2, magic2);
+        const float2 q = __fmul2_rn(d, inv2);
+        const float2 f = __fadd2_rn(q, __fadd2_rn(make_float2(-t.x, -t.y), magic2));  // q - round(q)
+        tie |= (fabsf(f.x) > kTieEdge) | (fabsf(f.y) > kTieEdge);
+        tb[i] = __float_as_uint(t.x);
+        tb[i + 1] = __float_as_uint(t.y);
+      }
+      uint32_t w0 = __byte_perm(__byte_perm(tb[0], tb[1], 0x0040), __byte_perm(tb[2], tb[3], 0x0040), 0x5410);
+      uint32_t w1 = __byte_perm(__byte_perm(tb[4], tb[5], 0x0040), __byte_perm(tb[6], tb[7], 0x0040), 0x5410);
+      const bool valid = rg * RT + rr < rows;
+      if (tie && valid) {  // rare: near a rounding tie or |mu| >> amax -> FP64 quotients for these 8
+        float xs[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) xs[i] = x[rr].get(i);
+        w0 = k_codes_exact8(xs, mu_g + c0, scale, inv, qmax, &w1);
+      }
+      if (!valid) w0 = w1 = 0u;
+      *reinterpret_cast<uint2*>(dst + rr * D) = make_uint2(w0, w1);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ pass 3: K/V blocks
+// One CTA (256 threads) per 64-key block of one (b, hkv).  Thread (rg, c8) holds channels
+// [8*c8, 8*c8+8) of the RT consecutive keys [rg*RT, rg*RT+RT) of both K and V in registers, so the
+// block is read from HBM exactly once and every output is produced from registers:
+//   k_codes  [B, Hkv, Np, D]          int8, 8-byte stores straight from registers
+//   v_codes  [B, Hkv, D, Np]          E4M3, transposed through a swizzled 64-byte-per-channel smem tile
+//   kv_meta  [B, Hkv, nKB, 4 + D]     f32 {dK, 0, 0, 0, dV[0..D)}
+//   bias     [B, Hq, Np]              f32 q_mean . Ks_j ; bias_l2 = bias * sm_scale * log2(e)
+// Per-channel statistics (K min/max, V |max|) are reduced across the row groups with shuffles and
+// across warps through shared memory; the block scalars need two CTA barriers, the transpose a third.
 template <typename T, int D>
 __host__ __device__ constexpr int kv_smem_bytes() {
   return 3 * 8 * D * 4 + D * 64 + D * 8 + D * 4 + 64;
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(256, 3) quantize_kv_kernel(InView kv_in, InView v_in, int Hq, int Hkv, int N, int Np,
+__global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InView v_in, int Hq, int Hkv, int N, int Np,
                                                              int n_kb, int qmax, double v_r, int smoothing,
                                                              double sm_scale_log2, const double* __restrict__ means,
                                                              int Ht, int8_t* __restrict__ k_codes,
@@ -551,7 +625,7 @@ __global__ void __launch_bounds__(256, 3) quantize_kv_kernel(InView kv_in, InVie
         const float2 q = __fmul2_rn(d, inv2);
         const float2 t = __fadd2_rn(q, magic2);
         const float2 f = __fadd2_rn(q, __fadd2_rn(make_float2(-t.x, -t.y), magic2));  // q - round(q)
-        tie |= (fabsf(f.x) > 0.4999f) | (fabsf(f.y) > 0.4999f);
+        tie |= (fabsf(f.x) > kTieEdge) | (fabsf(f.y) > kTieEdge);
         tb[i] = __float_as_uint(t.x);
         tb[i + 1] = __float_as_uint(t.y);
       }
@@ -686,9 +760,22 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
   } else {
     cudaMemsetAsync(L.means, 0, sizeof(double) * L.B * Ht * D, st);
   }
-  dim3 gq(L.n_qt, L.B * L.Hq);
-  quantize_q_kernel<T, D><<<gq, 256, 0, st>>>(qv, L.Hq, L.N, L.Nq_pad, L.n_qt, L.qmax, L.means, Ht, L.q_codes,
-                                              L.q_scale, L.q_scale64);
+  {  // persistent: as many CTAs as fit, each walking tiles with the next one in flight
+    constexpr int q_smem = q_smem_bytes<T, D>();
+    static int ctas_per_sm = 0;  // per template instance; benign race (idempotent)
+    if (ctas_per_sm == 0) {
+      cudaFuncSetAttribute(quantize_q_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, q_smem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, quantize_q_kernel<T, D>, 256, q_smem);
+      ctas_per_sm = ctas_per_sm < 1 ? 1 : ctas_per_sm;
+    }
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int n_tiles = L.n_qt * L.B * L.Hq;
+    const int grid = n_tiles < sms * ctas_per_sm ? n_tiles : sms * ctas_per_sm;
+    quantize_q_kernel<T, D><<<grid, 256, q_smem, st>>>(qv, L.Hq, L.N, L.Nq_pad, L.n_qt, n_tiles, L.qmax, L.means, Ht,
+                                                       L.q_codes, L.q_scale, L.q_scale64);
+  }
   dim3 gk(L.n_kb, L.B * L.Hkv);
   constexpr int kv_smem = kv_smem_bytes<T, D>();
   static bool attr_set = false;  // per template instance; benign race (idempotent)
