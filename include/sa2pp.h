@@ -167,6 +167,9 @@ SA2PP_API int sa2pp_host_pipeline_create(const sa2pp_problem* prob, int dtype, i
                                          sa2pp_host_pipeline** out);
 SA2PP_API int sa2pp_host_pipeline_run(sa2pp_host_pipeline* hp, const void* q, const void* k, const void* v, void* o,
                                       void* cuda_stream);
+/* Block the calling host thread until every call issued on `hp` has landed in host memory
+ * (for callers without a CUDA stream of their own, e.g. a numpy binding). */
+SA2PP_API int sa2pp_host_pipeline_sync(sa2pp_host_pipeline* hp);
 SA2PP_API int sa2pp_host_pipeline_destroy(sa2pp_host_pipeline* hp);
 
 /* Debug/introspection: dump raw TMEM of the first block of CTA 0 (S int32 [128,64] and

@@ -20,7 +20,7 @@ EXPORTED = (
     "sa2pp_version", "sa2pp_last_error", "sa2pp_check_problem", "sa2pp_quant_sizes",
     "sa2pp_prepass", "sa2pp_attn_fwd", "sa2pp_sageattn", "sa2pp_set_debug_buffer",
     "sa2pp_set_trace_buffer", "sa2pp_host_pipeline_create", "sa2pp_host_pipeline_run",
-    "sa2pp_host_pipeline_destroy",
+    "sa2pp_host_pipeline_sync", "sa2pp_host_pipeline_destroy",
 )
 
 
@@ -87,6 +87,7 @@ def lib() -> C.CDLL:
         h.sa2pp_set_trace_buffer.argtypes = [C.c_void_p]
         h.sa2pp_host_pipeline_create.argtypes = [P(Problem), C.c_int, C.c_int, C.c_int, P(C.c_void_p)]
         h.sa2pp_host_pipeline_run.argtypes = [C.c_void_p] * 6
+        h.sa2pp_host_pipeline_sync.argtypes = [C.c_void_p]
         h.sa2pp_host_pipeline_destroy.argtypes = [C.c_void_p]
         for name in EXPORTED[2:]:
             getattr(h, name).restype = C.c_int

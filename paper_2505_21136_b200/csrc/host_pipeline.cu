@@ -204,6 +204,15 @@ int sa2pp_host_pipeline_run(sa2pp_host_pipeline* hp, const void* q, const void* 
   return SA2PP_OK;
 }
 
+int sa2pp_host_pipeline_sync(sa2pp_host_pipeline* hp) {
+  if (!hp) return sa2pp::set_error(SA2PP_ERR_INVALID, "host pipeline handle is NULL");
+  DeviceGuard guard(hp->device);
+  cudaError_t e = cudaStreamSynchronize(hp->d2h);  // the last download of every issued chunk
+  if (e == cudaSuccess) e = cudaStreamSynchronize(hp->comp);
+  if (e != cudaSuccess) return sa2pp::set_error(SA2PP_ERR_CUDA, "host pipeline sync: %s", cudaGetErrorString(e));
+  return SA2PP_OK;
+}
+
 int sa2pp_host_pipeline_destroy(sa2pp_host_pipeline* hp) {
   release(hp);
   return SA2PP_OK;

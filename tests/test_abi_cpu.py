@@ -135,4 +135,5 @@ def test_host_pipeline_validates_before_touching_the_gpu():
     assert lib.sa2pp_host_pipeline_create(ctypes.byref(prob), A.SA2PP_BF16, 0, 2, ctypes.byref(h)) == A.SA2PP_ERR_INVALID
     assert h.value is None
     assert lib.sa2pp_host_pipeline_run(None, None, None, None, None, None) == A.SA2PP_ERR_INVALID
+    assert lib.sa2pp_host_pipeline_sync(None) == A.SA2PP_ERR_INVALID
     assert lib.sa2pp_host_pipeline_destroy(None) == A.SA2PP_OK

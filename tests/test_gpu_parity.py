@@ -235,6 +235,29 @@ def test_host_pipeline_back_to_back_calls(dtype):
     pipe.close()
 
 
+def test_host_pipeline_numpy_binding_through_the_c_abi():
+    """The reference-side binding INTEGRATION.md shows: float32 numpy arrays (pageable memory) in
+    and out through sa2pp_host_pipeline_create/run/sync/destroy, no torch tensors; equals the device
+    call on the same values (lpattn's attention_quantized takes and returns host arrays)."""
+    import ctypes
+    rng = np.random.Generator(np.random.Philox(5))
+    H, N, D = 3, 300, 64
+    q, k, v = (np.ascontiguousarray(rng.standard_normal((1, H, N, D)), dtype=np.float32) for _ in range(3))
+    out = np.empty_like(q)
+    lib = sa._abi.lib()
+    prob = sa.api._problem(1, H, H, N, D, causal=True)
+    h = ctypes.c_void_p()
+    sa._abi.check(lib.sa2pp_host_pipeline_create(ctypes.byref(prob), sa._abi.SA2PP_F32, 2, 2, ctypes.byref(h)))
+    try:
+        sa._abi.check(lib.sa2pp_host_pipeline_run(h, q.ctypes.data, k.ctypes.data, v.ctypes.data, out.ctypes.data,
+                                                  None))
+        sa._abi.check(lib.sa2pp_host_pipeline_sync(h))
+    finally:
+        lib.sa2pp_host_pipeline_destroy(h)
+    ref = sa.sageattn(*(torch.from_numpy(x).cuda() for x in (q, k, v)), "HND", True).cpu().numpy()
+    assert np.array_equal(out, ref)
+
+
 @pytest.mark.parametrize("d", [64, 128])
 @pytest.mark.parametrize("causal", [False, True])
 def test_ragged_lengths_vs_exact(d, causal):
