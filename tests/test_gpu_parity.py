@@ -163,31 +163,47 @@ def test_large_vs_exact_attention(causal, n):
     assert cos >= 0.999 and l1 <= 2e-2, (cos, l1)
 
 
-def test_headline_shape_properties():
-    """BASELINE configs[1] at full size (4 x 32 x 16384 x 128, bf16): the prepass codes, scales and bias of
-    sampled (batch, head) pairs bit-exact against the oracle port, their outputs against FP32 SDPA, and a
-    bit-identical rerun of the whole call."""
-    B, H, N, D = 4, 32, 16384, 128
+# BASELINE.json configs[1..4] at full size: (B, Hq, Hkv, N, D, causal), sampled (batch, q-head) pairs
+FULL_SHAPES = {
+    "kernel_16k": ((4, 32, 32, 16384, 128, False), ((0, 0), (3, 31))),
+    "cogvideox": ((2, 30, 30, 17776, 64, False), ((0, 0), (1, 29))),
+    "llama_gqa_causal": ((8, 32, 8, 8192, 128, True), ((0, 1), (7, 30))),
+    "longctx_128k_causal": ((1, 32, 32, 131072, 128, True), ((0, 5),)),
+}
+
+
+@pytest.mark.parametrize("name", sorted(FULL_SHAPES))
+def test_full_shape_properties(name):
+    """Each BASELINE workload at full size (bf16): the prepass codes, scales and bias of sampled
+    (batch, head) pairs bit-exact against the oracle port (GQA: the KV head of the group), their
+    outputs against FP32 SDPA, and a bit-identical rerun of the whole call."""
+    (B, H, Hkv, N, D, causal), samples = FULL_SHAPES[name]
     g = torch.Generator(device="cuda").manual_seed(2505)
     q = torch.randn(B, H, N, D, device="cuda", generator=g).bfloat16()
-    k = torch.randn(B, H, N, D, device="cuda", generator=g).bfloat16()
-    v = (torch.randn(B, H, N, D, device="cuda", generator=g)
-         + 2 * torch.randn(B, H, 1, D, device="cuda", generator=g)).bfloat16()
-    out, qt = sa.sageattn(q, k, v, return_quant=True)
-    assert torch.equal(out, sa.sageattn(q, k, v)), "rerun must be bit-identical"
-    cfg = oc.AttentionConfig(seq_len=N, head_dim=D, num_heads=1)
-    for b, h in ((0, 0), (3, 31)):
-        ref = oc.prepass(*(t[b, h].float().cpu().numpy() for t in (q, k, v)), cfg)
+    k = torch.randn(B, Hkv, N, D, device="cuda", generator=g).bfloat16()
+    v = (torch.randn(B, Hkv, N, D, device="cuda", generator=g)
+         + 2 * torch.randn(B, Hkv, 1, D, device="cuda", generator=g)).bfloat16()
+    out, qt = sa.sageattn(q, k, v, is_causal=causal, return_quant=True)
+    assert torch.equal(out, sa.sageattn(q, k, v, is_causal=causal)), "rerun must be bit-identical"
+    cfg = oc.AttentionConfig(seq_len=N, head_dim=D, num_heads=1, causal=causal)
+    for b, h in samples:
+        hk = h // (H // Hkv)
+        ref = oc.prepass(q[b, h].float().cpu().numpy(), k[b, hk].float().cpu().numpy(),
+                         v[b, hk].float().cpu().numpy(), cfg)
         assert np.array_equal(qt.q_codes[b, h].cpu().numpy()[:N], ref.q_codes)
         assert np.array_equal(qt.q_scale64[b, h].cpu().numpy(), ref.q_scale)
-        assert np.array_equal(qt.k_codes[b, h].cpu().numpy(), ref.k_codes)
-        assert np.array_equal(qt.k_scale64[b, h].cpu().numpy(), ref.k_scale)
-        assert np.array_equal(qt.v_codes[b, h].cpu().numpy().T, ref.v_codes)
-        assert np.array_equal(qt.v_scale64[b, h].cpu().numpy(), ref.v_scale)
+        assert np.array_equal(qt.k_codes[b, hk].cpu().numpy(), ref.k_codes)
+        assert np.array_equal(qt.k_scale64[b, hk].cpu().numpy(), ref.k_scale)
+        assert np.array_equal(qt.v_codes[b, hk].cpu().numpy().T, ref.v_codes)
+        assert np.array_equal(qt.v_scale64[b, hk].cpu().numpy(), ref.v_scale)
         assert f32_ulp_close(qt.bias[b, h].cpu().numpy(), ref.bias)
-        exact = torch.nn.functional.scaled_dot_product_attention(*(t[b, h][None, None].float() for t in (q, k, v)))
+        exact = torch.nn.functional.scaled_dot_product_attention(
+            q[b, h][None, None].float(), k[b, hk][None, None].float(), v[b, hk][None, None].float(),
+            is_causal=causal)
         cos, l1, _ = sa.compare(exact[0, 0].cpu().numpy(), out[b, h].float().cpu().numpy())
         assert cos >= 0.999 and l1 <= 2e-2, (b, h, cos, l1)
+    del out, qt, q, k, v
+    torch.cuda.empty_cache()
 
 
 def test_fp32_accumulator_close_to_fp16():
