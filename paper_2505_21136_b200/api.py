@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _abi as A
-from .config import AttentionConfig, RangeConfig
+from .config import AttentionConfig
 
 _DT = {torch.float32: A.SA2PP_F32, torch.float16: A.SA2PP_F16, torch.bfloat16: A.SA2PP_BF16}
 
