@@ -137,3 +137,13 @@ def test_host_pipeline_validates_before_touching_the_gpu():
     assert lib.sa2pp_host_pipeline_run(None, None, None, None, None, None) == A.SA2PP_ERR_INVALID
     assert lib.sa2pp_host_pipeline_sync(None) == A.SA2PP_ERR_INVALID
     assert lib.sa2pp_host_pipeline_destroy(None) == A.SA2PP_OK
+
+
+def test_conversion_halving_counters():
+    """lpattn tests/test_attention.py:217-230 on the analytic RunReport counters the mirror reports:
+    depth 1 converts every k=32 group sum, depth 2 every pair, MMA invocations are unchanged."""
+    from paper_2505_21136_b200.api import _analytic_counts
+    counts = {d: _analytic_counts(sa.AttentionConfig(seq_len=128, head_dim=32, range=sa.RangeConfig(224.0, 4.5, d)))
+              for d in (1, 2)}
+    assert counts[1][0] == 2 * counts[2][0]
+    assert counts[1][1] == counts[2][1]
