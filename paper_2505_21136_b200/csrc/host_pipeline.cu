@@ -34,6 +34,8 @@ struct sa2pp_host_pipeline {
   cudaEvent_t done = nullptr;
   long long ring = 0;  // chunks issued over the handle's lifetime; buffer set = ring % depth
 };
+// A handle is not thread-safe: one host thread issues its calls (the ring index is unsynchronised).
+// Copies use cudaMemcpyDefault (UVA), so device-resident inputs/outputs also work (as D2D copies).
 
 namespace {
 
@@ -166,9 +168,9 @@ int sa2pp_host_pipeline_run(sa2pp_host_pipeline* hp, const void* q, const void* 
     const int s = static_cast<int>(hp->ring % hp->depth);
     const sa2pp_host_pipeline::Set& S = hp->sets[s];
     if (hp->ring >= hp->depth) e = cudaStreamWaitEvent(hp->h2d, hp->ev_out[s], 0);  // set s drained
-    if (e == cudaSuccess) e = cudaMemcpyAsync(S.q, qh + u0 * hp->q_unit, n * hp->q_unit, cudaMemcpyHostToDevice, hp->h2d);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(S.k, kh + u0 * hp->kv_unit, n * hp->kv_unit, cudaMemcpyHostToDevice, hp->h2d);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(S.v, vh + u0 * hp->kv_unit, n * hp->kv_unit, cudaMemcpyHostToDevice, hp->h2d);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(S.q, qh + u0 * hp->q_unit, n * hp->q_unit, cudaMemcpyDefault, hp->h2d);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(S.k, kh + u0 * hp->kv_unit, n * hp->kv_unit, cudaMemcpyDefault, hp->h2d);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(S.v, vh + u0 * hp->kv_unit, n * hp->kv_unit, cudaMemcpyDefault, hp->h2d);
     if (e == cudaSuccess) e = cudaEventRecord(hp->ev_in[s], hp->h2d);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(hp->comp, hp->ev_in[s], 0);
     if (e != cudaSuccess) break;
@@ -194,7 +196,7 @@ int sa2pp_host_pipeline_run(sa2pp_host_pipeline* hp, const void* q, const void* 
     if (rc) return rc;
     e = cudaEventRecord(hp->ev_comp[s], hp->comp);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(hp->d2h, hp->ev_comp[s], 0);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(oh + u0 * hp->q_unit, S.o, n * hp->q_unit, cudaMemcpyDeviceToHost, hp->d2h);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(oh + u0 * hp->q_unit, S.o, n * hp->q_unit, cudaMemcpyDefault, hp->d2h);
     if (e == cudaSuccess) e = cudaEventRecord(hp->ev_out[s], hp->d2h);
     ++hp->ring;
   }
