@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(256, 2)
         tmem_ld16_pack16(tm_row + 128 + h * HD + c0, v);  // F16 accumulators, 2 per register
         tmem_wait_ld();
 #pragma unroll
-        for (int i = 0; i < CH / 2; ++i) pv[i] = __half22float2(*reinterpret_cast<const __half2*>(&v[i]));
+        for (int i = 0; i < CH / 2; ++i) pv[i] = f16x2_to_f32x2(v[i]);
         if (want_overflow) {
 #pragma unroll
           for (int i = 0; i < CH / 2; ++i)

@@ -199,6 +199,14 @@ __host__ __device__ constexpr uint32_t make_idesc(uint32_t c_fmt, uint32_t a_fmt
   return (c_fmt << 4) | (a_fmt << 7) | (b_fmt << 10) | ((N >> 3) << 17) | ((M >> 4) << 24);
 }
 
+// f16x2 -> two f32 on the FMA pipe: mixed-precision add (FHADD, sm_100) of -0.0, exact for every input
+// (x + -0 = x, including +-0, inf and NaN); HADD2.F32 would do the same on the half-rate ALU pipe.
+__device__ __forceinline__ float2 f16x2_to_f32x2(uint32_t v) {
+  float2 r;
+  asm("{.reg .f16 l, h;\n\tmov.b32 {l, h}, %2;\n\tadd.rn.f32.f16 %0, l, %3;\n\tadd.rn.f32.f16 %1, h, %3;}"
+      : "=f"(r.x), "=f"(r.y) : "r"(v), "f"(-0.0f));
+  return r;
+}
 __device__ __forceinline__ void umma_i8_ss(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                            uint32_t accumulate) {
   asm volatile(
