@@ -239,14 +239,27 @@ template <typename T>
 struct KvTile {
   static constexpr int kWords = 8 * static_cast<int>(sizeof(T)) / 4;  // 32-bit words per 8 channels
   uint32_t w[kWords];
+  // 16-bit -> f32 on the FMA pipe: the sm_100 mixed-precision add of -0.0 (FHADD / FHADD.BF16), exact
+  // for every input; shifts/masks or HADD2.F32 would load the half-rate ALU pipe these kernels lean on.
   __device__ __forceinline__ float get(int i) const {
     if constexpr (sizeof(T) == 4) {
       return __uint_as_float(w[i]);
-    } else if constexpr (std::is_same<T, __nv_bfloat16>::value) {
-      return __uint_as_float((i & 1) ? (w[i >> 1] & 0xFFFF0000u) : (w[i >> 1] << 16));
     } else {
-      const __half2 h = *reinterpret_cast<const __half2*>(&w[i >> 1]);
-      return (i & 1) ? __high2float(h) : __low2float(h);
+      float r;
+      if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        if (i & 1) {
+          asm("{.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.bf16 %0, h, %2;}" : "=f"(r) : "r"(w[i >> 1]), "f"(-0.0f));
+        } else {
+          asm("{.reg .b16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.bf16 %0, l, %2;}" : "=f"(r) : "r"(w[i >> 1]), "f"(-0.0f));
+        }
+      } else {
+        if (i & 1) {
+          asm("{.reg .f16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.f16 %0, h, %2;}" : "=f"(r) : "r"(w[i >> 1]), "f"(-0.0f));
+        } else {
+          asm("{.reg .f16 l, h;\n\tmov.b32 {l, h}, %1;\n\tadd.rn.f32.f16 %0, l, %2;}" : "=f"(r) : "r"(w[i >> 1]), "f"(-0.0f));
+        }
+      }
+      return r;
     }
   }
   __device__ __forceinline__ float2 get2(int i) const { return make_float2(get(i), get(i + 1)); }
