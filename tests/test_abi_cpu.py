@@ -147,3 +147,13 @@ def test_conversion_halving_counters():
               for d in (1, 2)}
     assert counts[1][0] == 2 * counts[2][0]
     assert counts[1][1] == counts[2][1]
+
+
+def test_integration_stub_is_valid_python_and_binds_declared_symbols():
+    """The reference-side binding shown in INTEGRATION.md compiles and only names C entry points that
+    include/sa2pp.h declares."""
+    text = (ROOT / "INTEGRATION.md").read_text()
+    block = re.search(r"```python\n(# lpattn/_b200\.py.*?)```", text, re.S).group(1)
+    compile(block, "INTEGRATION.md", "exec")
+    used = set(re.findall(r"\b(sa2pp_\w+)", block)) | {f"sa2pp_host_pipeline_{f}" for f in ("create", "run", "sync", "destroy")}
+    assert used <= set(declared_functions()) | {"sa2pp_host_pipeline_"}, used - set(declared_functions())
