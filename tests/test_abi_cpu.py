@@ -155,5 +155,9 @@ def test_integration_stub_is_valid_python_and_binds_declared_symbols():
     text = (ROOT / "INTEGRATION.md").read_text()
     block = re.search(r"```python\n(# lpattn/_b200\.py.*?)```", text, re.S).group(1)
     compile(block, "INTEGRATION.md", "exec")
-    used = set(re.findall(r"\b(sa2pp_\w+)", block)) | {f"sa2pp_host_pipeline_{f}" for f in ("create", "run", "sync", "destroy")}
-    assert used <= set(declared_functions()) | {"sa2pp_host_pipeline_"}, used - set(declared_functions())
+    header = (ROOT / "include" / "sa2pp.h").read_text()
+    called = set(re.findall(r"_lib\.(sa2pp_\w+)\(", block))
+    called |= {f"sa2pp_host_pipeline_{f}" for f in re.findall(r'for _f in \(([^)]*)\)', block)[0].replace('"', "").replace(" ", "").split(",") if f}
+    assert called and called <= set(declared_functions()), called - set(declared_functions())
+    for name in re.findall(r"#.*?\b(sa2pp_[a-z_]+)\b", block):  # types named in comments exist too
+        assert name in header, name
