@@ -66,7 +66,7 @@ typedef struct {
   int32_t pv_accum;       /* sa2pp_accum: FP16 (default, SageAttention2++) or FP32 */
   int32_t buffering_depth;/* 2 (default): the two k=32 group sums of a 64-key block combine in FP16 */
   int32_t expect_overflow;/* waiver for unsafe range pairs (quantization.py:47) */
-  double sm_scale;        /* <= 0 selects 1/sqrt(head_dim) (attention.py:87-91) */
+  double sm_scale;        /* NaN selects 1/sqrt(head_dim) (attention.py:87-91); any finite value is used as given */
   double p_r;             /* default 224.0 */
   double v_r;             /* default 4.5   */
 } sa2pp_problem;
@@ -111,7 +111,7 @@ typedef struct {
 
 typedef struct {
   size_t q_codes, q_scale, q_scale64, k_codes, v_codes, kv_meta, kv_scale64, bias, bias_l2, means;
-  size_t workspace; /* scratch for the FP64 channel sums */
+  size_t workspace; /* reserved scratch (0 bytes with the current kernels) */
 } sa2pp_quant_sizes_t;
 
 /* Output [.., D] with element strides for (batch, head, token), same dtype choices as inputs. */

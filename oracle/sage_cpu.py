@@ -343,6 +343,65 @@ def _n_visible(cfg: AttentionConfig, q_stop: int, nkb: int) -> int:
     return min(nkb, -(-q_stop // cfg.block_k)) if cfg.causal else nkb
 
 
+@dataclass
+class TileStats:
+    overflow: int = 0
+    conversions: int = 0
+    mma: int = 0
+    p_scales: list = field(default_factory=list)
+
+
+def attention_tile(qt: QuantizedTensors, cfg: AttentionConfig, i: int, stats: TileStats | None = None) -> np.ndarray:
+    """Output rows of query tile i of one head from its prepass tensors: the body of the reference's
+    tile loop (attention.py:282-305).  Used by attention_quantized and, on sampled tiles of full-size
+    heads, by the GPU parity tests."""
+    n, d, bq, bk = cfg.seq_len, cfg.head_dim, cfg.block_q, cfg.block_k
+    sm = cfg.scale
+    depth = cfg.range.buffering_depth
+    st = stats if stats is not None else TileStats()
+    nkb = qt.k_codes.shape[0] // bk
+    i0 = i * bq
+    i1 = min(i0 + bq, n)
+    rows = i1 - i0
+    qc = qt.q_codes[i0:i1].astype(np.int64)
+    m_run = np.full(rows, -np.inf)
+    l_run = np.zeros(rows)
+    o_run = np.zeros((rows, d))
+    for j in range(_n_visible(cfg, i1, nkb)):
+        j0, j1 = j * bk, (j + 1) * bk
+        s_int = qc @ qt.k_codes[j0:j1].astype(np.int64).T
+        st.mma += rows * bk * (-(-d // K_GROUP))
+        s = s_int * (qt.q_scale[i] * qt.k_scale[j])
+        if cfg.smoothing:
+            s = s + qt.q_mean @ qt.k_smoothed[j0:j1].T
+        s = s * sm
+        if cfg.causal:
+            qi = np.arange(i0, i1)[:, None]
+            kj = np.arange(j0, j1)[None, :]
+            s = np.where(kj > qi, NEG_INF, s)
+        if j1 > n:
+            s[:, n - j0:] = NEG_INF
+        # online softmax (attention.py:136-154)
+        m_new = np.maximum(m_run, s.max(axis=1))
+        p = np.exp(s - m_new[:, None])
+        alpha = np.exp(m_run - m_new)
+        l_run = l_run * alpha + p.sum(axis=1)
+        o_run = o_run * alpha[:, None]
+        m_run = m_new
+        p_codes, p_scale = p_quantize(p, cfg.range.p_r)
+        st.p_scales.append(p_scale)
+        if cfg.pv_accumulator == "fp16":
+            pv, ov, cv = fp8_gemm_fp16acc(p_codes, qt.v_codes[j0:j1], depth)
+            st.overflow += ov
+            st.conversions += cv
+        else:
+            pv = fp8_gemm_fp32acc(p_codes, qt.v_codes[j0:j1])
+        st.mma += rows * d * (bk // K_GROUP)
+        o_run = o_run + pv.astype(np.float64) * (p_scale * qt.v_scale[j])
+    l_safe = np.where(l_run == 0.0, 1.0, l_run)
+    return o_run / l_safe[:, None]
+
+
 def attention_quantized(q, k, v, cfg: AttentionConfig) -> RunReport:
     """The reference operator (attention.py:232-316), head by head."""
     if cfg.head_dim % K_GROUP or cfg.block_k % K_GROUP:
@@ -350,59 +409,17 @@ def attention_quantized(q, k, v, cfg: AttentionConfig) -> RunReport:
     squeeze = np.ndim(q) == 2
     q3, k3, v3 = (_as_heads(t, cfg) for t in (q, k, v))
     out = np.empty_like(q3)
-    n, d, bq, bk = cfg.seq_len, cfg.head_dim, cfg.block_q, cfg.block_k
-    sm = cfg.scale
-    depth = cfg.range.buffering_depth
-    overflow = conversions = mma = 0
-    p_scales: list[float] = []
+    n, bq = cfg.seq_len, cfg.block_q
+    st = TileStats()
     v_lo, v_hi = math.inf, -math.inf
     for h in range(cfg.num_heads):
         qt = prepass(q3[h], k3[h], v3[h], cfg)
-        nkb = qt.k_codes.shape[0] // bk
         v_lo = min(v_lo, float(qt.v_scale.min()))
         v_hi = max(v_hi, float(qt.v_scale.max()))
         for i, i0 in enumerate(range(0, n, bq)):
-            i1 = min(i0 + bq, n)
-            rows = i1 - i0
-            qc = qt.q_codes[i0:i1].astype(np.int64)
-            m_run = np.full(rows, -np.inf)
-            l_run = np.zeros(rows)
-            o_run = np.zeros((rows, d))
-            for j in range(_n_visible(cfg, i1, nkb)):
-                j0, j1 = j * bk, (j + 1) * bk
-                s_int = qc @ qt.k_codes[j0:j1].astype(np.int64).T
-                mma += rows * bk * (-(-d // K_GROUP))
-                s = s_int * (qt.q_scale[i] * qt.k_scale[j])
-                if cfg.smoothing:
-                    s = s + qt.q_mean @ qt.k_smoothed[j0:j1].T
-                s = s * sm
-                if cfg.causal:
-                    qi = np.arange(i0, i1)[:, None]
-                    kj = np.arange(j0, j1)[None, :]
-                    s = np.where(kj > qi, NEG_INF, s)
-                if j1 > n:
-                    s[:, n - j0:] = NEG_INF
-                # online softmax (attention.py:136-154)
-                m_new = np.maximum(m_run, s.max(axis=1))
-                p = np.exp(s - m_new[:, None])
-                alpha = np.exp(m_run - m_new)
-                l_run = l_run * alpha + p.sum(axis=1)
-                o_run = o_run * alpha[:, None]
-                m_run = m_new
-                p_codes, p_scale = p_quantize(p, cfg.range.p_r)
-                p_scales.append(p_scale)
-                if cfg.pv_accumulator == "fp16":
-                    pv, ov, cv = fp8_gemm_fp16acc(p_codes, qt.v_codes[j0:j1], depth)
-                    overflow += ov
-                    conversions += cv
-                else:
-                    pv = fp8_gemm_fp32acc(p_codes, qt.v_codes[j0:j1])
-                mma += rows * d * (bk // K_GROUP)
-                o_run = o_run + pv.astype(np.float64) * (p_scale * qt.v_scale[j])
-            l_safe = np.where(l_run == 0.0, 1.0, l_run)
-            out[h, i0:i1] = o_run / l_safe[:, None]
-    return RunReport(out[0] if squeeze else out, overflow, conversions, mma,
-                     min(p_scales), max(p_scales), v_lo, v_hi)
+            out[h, i0:min(i0 + bq, n)] = attention_tile(qt, cfg, i, st)
+    return RunReport(out[0] if squeeze else out, st.overflow, st.conversions, st.mma,
+                     min(st.p_scales), max(st.p_scales), v_lo, v_hi)
 
 
 def attention_reference(q, k, v, cfg: AttentionConfig) -> np.ndarray:

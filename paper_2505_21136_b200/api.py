@@ -54,7 +54,7 @@ def _problem(B, Hq, Hkv, N, D, *, causal, smoothing=True, qk_bits=8, pv_accum="f
              expect_overflow=False, sm_scale=None, p_r=224.0, v_r=4.5) -> A.Problem:
     return A.Problem(B, Hq, Hkv, N, D, int(bool(causal)), int(bool(smoothing)), qk_bits,
                      A.SA2PP_ACC_F16 if pv_accum == "fp16" else A.SA2PP_ACC_F32, depth,
-                     int(bool(expect_overflow)), float(sm_scale) if sm_scale else 0.0,
+                     int(bool(expect_overflow)), float("nan") if sm_scale is None else float(sm_scale),
                      float(p_r), float(v_r))
 
 

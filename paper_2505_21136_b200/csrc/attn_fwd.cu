@@ -593,14 +593,13 @@ static cudaError_t launch_t(const AttnParams& P, const sa2pp_quant& qt, cudaStre
                    CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
   auto kern = attn_fwd_kernel<D, CAUSAL, ACC16, INSTR, OutT>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static PerDevice once;
+  cudaError_t e = once.run([&](std::atomic<int>&) {
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return r;
+  });
+  if (e != cudaSuccess) return e;
   dim3 grid(P.n_qt, P.B * P.Hq);
   kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(mq, mk, mv, P);
   return cudaGetLastError();

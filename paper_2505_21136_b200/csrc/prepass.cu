@@ -10,8 +10,7 @@
 // Arithmetic is FP64 with RNE division, exactly as the reference's numpy float64.
 //
 // Kernels:
-//   channel_sums   grid (chunks, B*(Hq+Hkv))  double-double partial sums over token chunks
-//   channel_means  grid (B*(Hq+Hkv))          fixed-order reduction of the partials -> FP64 mean
+//   channel_means  grid (B*(Hq+Hkv))          sequential FP64 channel sums in token order -> mean
 //   quantize_q     grid (nQT, B*Hq)           one CTA per 128-row query tile
 //   quantize_kv    grid (nKB, B*Hkv)          one CTA per 64-key block (K codes, V^T codes, scales, bias)
 #include <cuda_bf16.h>
@@ -34,19 +33,6 @@ __device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 x) {
   return static_cast<double>(__bfloat162float(x));
 }
 
-// Error-free transformation: s + e == a + b exactly.
-__device__ __forceinline__ void two_sum(double a, double b, double& s, double& e) {
-  s = a + b;
-  double bb = s - a;
-  e = (a - (s - bb)) + (b - bb);
-}
-__device__ __forceinline__ void dd_add(double& hi, double& lo, double x) {
-  double s, e;
-  two_sum(hi, x, s, e);
-  lo += e;
-  hi = s;
-}
-
 template <typename T>
 __device__ __forceinline__ float to_f32(T x);
 template <>
@@ -67,96 +53,95 @@ __device__ __forceinline__ const T* row_ptr(const InView& v, int b, int h, int n
   return static_cast<const T*>(v.base) + b * v.sb + h * v.sh + static_cast<int64_t>(n) * v.sn;
 }
 
-// ------------------------------------------------------------------ pass 1: channel sums
-// blockDim = 256; thread t owns channels [c8*VEC, c8*VEC+VEC) of rows t/(D/VEC) + k*stride.
+// ------------------------------------------------------------------ pass 1: channel means
+// numpy's x.mean(axis=0) over a C-ordered (N, D) float64 array is a SEQUENTIAL float64 sum per
+// channel in token order followed by one division by N (quantization.py:133,147; checked against
+// numpy in tests/test_gpu_parity.py), so each channel is one FP64 add chain here too: one CTA per
+// (b, head) of Q and K, thread t owns channels {2t, 2t+1}; the head's rows stream through a 4-stage
+// cp.async ring in shared memory (16 KB per stage) and every thread adds its two channels row by row.
 template <typename T, int D>
-__global__ void __launch_bounds__(256) channel_sums_kernel(InView qv, InView kv, int Hq, int Hkv, int N,
-                                                           int rows_per_chunk, double2* __restrict__ partial,
-                                                           int n_chunks) {
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int LANES_PER_ROW = D / VEC;
-  constexpr int ROWS_PER_PASS = 256 / LANES_PER_ROW;
-  const int chunk = blockIdx.x;
-  const int bh = blockIdx.y;  // in [0, B*(Hq+Hkv))
-  const int Ht = Hq + Hkv;
-  const int b = bh / Ht;
-  const int h = bh % Ht;
-  const InView& v = (h < Hq) ? qv : kv;
-  const int hh = (h < Hq) ? h : h - Hq;
-  const int c8 = threadIdx.x % LANES_PER_ROW;
-  const int r0 = threadIdx.x / LANES_PER_ROW;
-  const int n_begin = chunk * rows_per_chunk;
-  const int n_end = min(N, n_begin + rows_per_chunk);
-  double hi[VEC], lo[VEC];
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) hi[i] = lo[i] = 0.0;
-  // The next U rows stream into shared memory with cp.async (no registers held, so the compiler
-  // cannot sink the loads behind the FP64 chain) while the current U rows are summed.  Every thread
-  // reads back only its own copies: cp.async.wait_group is the only synchronisation.  Rows past the
-  // chunk are zero-filled, which adds exactly nothing.
-  constexpr int U = 4;
-  __shared__ __align__(16) uint4 smem_cs[2 * U * 256];  // 32 KB; reused by the combine below
-  auto issue = [&](int n0, int slot) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int n = n0 + u * ROWS_PER_PASS;
-      const T* src = row_ptr<T>(v, b, hh, n < n_end ? n : n_begin) + c8 * VEC;
-      const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&smem_cs[(slot * U + u) * 256 + threadIdx.x]));
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(n < n_end ? 16 : 0)
-                   : "memory");
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  issue(n_begin + r0, 0);
-  int slot = 0;
-  for (int n = n_begin + r0; n < n_end; n += U * ROWS_PER_PASS) {
-    issue(n + U * ROWS_PER_PASS, slot ^ 1);
-    asm volatile("cp.async.wait_group 1;" ::: "memory");
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint4 raw = smem_cs[(slot * U + u) * 256 + threadIdx.x];
-      const T* e = reinterpret_cast<const T*>(&raw);
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) dd_add(hi[i], lo[i], to_f64<T>(e[i]));
-    }
-    slot ^= 1;
-  }
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();
-  // Fixed-order combine of the ROWS_PER_PASS row-groups through shared memory.
-  static_assert(sizeof(double2) * 256 * VEC <= sizeof(smem_cs), "combine buffer fits the staging buffer");
-  double2* red = reinterpret_cast<double2*>(smem_cs);
-#pragma unroll
-  for (int i = 0; i < VEC; ++i) red[threadIdx.x * VEC + i] = make_double2(hi[i], lo[i]);
-  __syncthreads();
-  if (threadIdx.x < LANES_PER_ROW) {
-#pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      double H = 0.0, L = 0.0;
-      for (int r = 0; r < ROWS_PER_PASS; ++r) {
-        const double2 p = red[(r * LANES_PER_ROW + threadIdx.x) * VEC + i];
-        dd_add(H, L, p.x);
-        L += p.y;
-      }
-      partial[(static_cast<int64_t>(bh) * n_chunks + chunk) * D + threadIdx.x * VEC + i] = make_double2(H, L);
-    }
+struct MeansCfg {
+  static constexpr int kThreads = D / 2;
+  static constexpr int kRowBytes = D * static_cast<int>(sizeof(T));
+  static constexpr int kStageBytes = 16384;
+  static constexpr int kRows = kStageBytes / kRowBytes;  // rows per stage
+  static constexpr int kStages = 4;
+  static constexpr int kPieces = kStageBytes / 16 / kThreads;  // 16-byte cp.async per thread per stage
+};
+
+template <typename T>
+__device__ __forceinline__ void two_f64(const void* p, double& a, double& b) {
+  if constexpr (sizeof(T) == 4) {
+    const float2 f = *reinterpret_cast<const float2*>(p);
+    a = static_cast<double>(f.x);
+    b = static_cast<double>(f.y);
+  } else if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+    a = static_cast<double>(__uint_as_float(w << 16));
+    b = static_cast<double>(__uint_as_float(w & 0xFFFF0000u));
+  } else {
+    const __half2 h = *reinterpret_cast<const __half2*>(p);
+    a = static_cast<double>(__low2float(h));
+    b = static_cast<double>(__high2float(h));
   }
 }
 
-// ------------------------------------------------------------------ pass 1b: means
-template <int D>
-__global__ void channel_means_kernel(const double2* __restrict__ partial, int n_chunks, int N,
-                                     double* __restrict__ means) {
-  const int bh = blockIdx.x;
-  for (int c = threadIdx.x; c < D; c += blockDim.x) {
-    double H = 0.0, L = 0.0;
-    for (int k = 0; k < n_chunks; ++k) {
-      const double2 p = partial[(static_cast<int64_t>(bh) * n_chunks + k) * D + c];
-      dd_add(H, L, p.x);
-      L += p.y;
+template <typename T, int D>
+__global__ void __launch_bounds__(D / 2) channel_means_kernel(InView qv, InView kv, int Hq, int Hkv, int N,
+                                                              double* __restrict__ means) {
+  using M = MeansCfg<T, D>;
+  extern __shared__ __align__(16) unsigned char ms_smem[];
+  const int bh = blockIdx.x;  // in [0, B*(Hq+Hkv))
+  const int Ht = Hq + Hkv;
+  const int b = bh / Ht, h = bh % Ht;
+  const InView& v = (h < Hq) ? qv : kv;
+  const int hh = (h < Hq) ? h : h - Hq;
+  const int t = threadIdx.x;
+  const int n_st = (N + M::kRows - 1) / M::kRows;
+  auto issue = [&](int s) {
+    if (s < n_st) {
+      unsigned char* dst = ms_smem + (s % M::kStages) * M::kStageBytes;
+#pragma unroll
+      for (int i = 0; i < M::kPieces; ++i) {
+        const int piece = i * M::kThreads + t;  // 16-byte piece of the stage
+        const int r = piece / (M::kRowBytes / 16), c16 = piece % (M::kRowBytes / 16);
+        const int n = s * M::kRows + r;
+        const unsigned char* src = reinterpret_cast<const unsigned char*>(row_ptr<T>(v, b, hh, n < N ? n : 0)) + 16 * c16;
+        const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + 16 * piece));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n < N ? 16 : 0) : "memory");
+      }
     }
-    means[static_cast<int64_t>(bh) * D + c] = (H + L) / static_cast<double>(N);
+    asm volatile("cp.async.commit_group;" ::: "memory");  // empty groups keep the wait count uniform
+  };
+#pragma unroll
+  for (int s = 0; s < M::kStages - 1; ++s) issue(s);
+  double s0 = 0.0, s1 = 0.0;
+  for (int s = 0; s < n_st; ++s) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(M::kStages - 2) : "memory");
+    __syncthreads();  // stage s landed for every thread; stage s-1 is no longer read
+    issue(s + M::kStages - 1);
+    const unsigned char* src = ms_smem + (s % M::kStages) * M::kStageBytes + t * 2 * sizeof(T);
+    const int rows = min(M::kRows, N - s * M::kRows);
+    if (rows == M::kRows) {
+#pragma unroll 16
+      for (int r = 0; r < M::kRows; ++r) {
+        double a, c;
+        two_f64<T>(src + r * M::kRowBytes, a, c);
+        s0 += a;
+        s1 += c;
+      }
+    } else {
+      for (int r = 0; r < rows; ++r) {
+        double a, c;
+        two_f64<T>(src + r * M::kRowBytes, a, c);
+        s0 += a;
+        s1 += c;
+      }
+    }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  const double n = static_cast<double>(N);
+  *reinterpret_cast<double2*>(means + static_cast<int64_t>(bh) * D + 2 * t) = make_double2(s0 / n, s1 / n);
 }
 
 // ------------------------------------------------------------------ shared helpers
@@ -425,7 +410,7 @@ __global__ void __launch_bounds__(256, 2) quantize_q_kernel(InView qv, int Hq, i
     }
     const double inv = 1.0 / scale;
     const float inv32 = static_cast<float>(inv);
-    const bool fast = mumax <= 65536.0 * amax;  // the error bound of the FP32 fast path
+    const bool fast = mumax <= 65536.0 * amax && amax >= 0x1p-100;  // see quantize_kv
 
     // codes: ((q - mu_hi) - mu_lo) * inv rounded with the 1.5*2^23 trick; the code is the low byte
     // of the rounded float's bits (|q| <= qmax + 3e-5 under `fast`, so no clamp is needed)
@@ -586,7 +571,9 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InVie
     double mumax = fabs(mu);
     const double sc = va > 0.0f ? static_cast<double>(va) / v_r : 1.0;
     s_vsc[tid] = sc;
-    s_vinv[tid] = static_cast<float>(1.0 / sc);
+    // a channel whose block max is below 2^-100 (its f32 reciprocal may overflow, its quotients may
+    // be subnormal) is encoded from the FP64 quotients; NaN marks it for the exact path below
+    s_vinv[tid] = (va > 0.0f && va < 0x1p-100f) ? __int_as_float(0x7fffffff) : static_cast<float>(1.0 / sc);
     meta[4 + tid] = static_cast<float>(sc);
     sc64[1 + tid] = sc;
 #pragma unroll
@@ -609,7 +596,9 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InVie
   const double kscale = amax > 0.0 ? amax / static_cast<double>(qmax) : 1.0;
   const double kinv = 1.0 / kscale;
   const float kinv32 = static_cast<float>(kinv);
-  const bool kfast = mumax <= 65536.0 * amax;  // the error bound of the FP32 fast path
+  // the error bound of the FP32 fast path; amax >= 2^-100 keeps the f32 reciprocal finite and the
+  // absolute error of subnormal intermediates (2^-150) far below a code step
+  const bool kfast = mumax <= 65536.0 * amax && amax >= 0x1p-100;
   if (tid < 4) meta[tid] = tid == 0 ? static_cast<float>(kscale) : 0.0f;
   if (tid == 0) sc64[0] = kscale;
 
@@ -667,6 +656,8 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InVie
     for (int i = 0; i < 8; ++i) {
       const int c = c0 + i;
       const float inv = s_vinv[c];
+      const uint32_t all_exact = isnan(inv) ? ((1u << RT) - 1u) << (i * RT) : 0u;
+      tmask |= all_exact;
       uint32_t unit = 0u;
 #pragma unroll
       for (int rr = 0; rr < RT; rr += 2) {
@@ -766,24 +757,32 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
   InView vv{L.v, L.v_stride[0], L.v_stride[1], L.v_stride[2]};
   const int Ht = L.Hq + L.Hkv;
   if (L.smoothing) {
-    dim3 g1(L.n_chunks, L.B * Ht);
-    channel_sums_kernel<T, D><<<g1, 256, 0, st>>>(qv, kv, L.Hq, L.Hkv, L.N, L.rows_per_chunk, L.partial,
-                                                  L.n_chunks);
-    channel_means_kernel<D><<<L.B * Ht, 128, 0, st>>>(L.partial, L.n_chunks, L.N, L.means);
+    using M = MeansCfg<T, D>;
+    constexpr int smem = M::kStages * M::kStageBytes;
+    static PerDevice once;
+    cudaError_t e = once.run([&](std::atomic<int>&) {
+      return cudaFuncSetAttribute(channel_means_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    });
+    if (e != cudaSuccess) return e;
+    channel_means_kernel<T, D><<<L.B * Ht, M::kThreads, smem, st>>>(qv, kv, L.Hq, L.Hkv, L.N, L.means);
   } else {
     cudaMemsetAsync(L.means, 0, sizeof(double) * L.B * Ht * D, st);
   }
   {  // persistent: as many CTAs as fit, each walking tiles with the next one in flight
     constexpr int q_smem = q_smem_bytes<T, D>();
-    static int ctas_per_sm = 0;  // per template instance; benign race (idempotent)
-    if (ctas_per_sm == 0) {
-      cudaFuncSetAttribute(quantize_q_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, q_smem);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, quantize_q_kernel<T, D>, 256, q_smem);
-      ctas_per_sm = ctas_per_sm < 1 ? 1 : ctas_per_sm;
-    }
+    static PerDevice occ;
+    cudaError_t e = occ.run([&](std::atomic<int>& v) {
+      cudaError_t r = cudaFuncSetAttribute(quantize_q_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, q_smem);
+      int n = 0;
+      if (r == cudaSuccess) r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, quantize_q_kernel<T, D>, 256, q_smem);
+      v.store(n < 1 ? 1 : n);
+      return r;
+    });
+    if (e != cudaSuccess) return e;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int ctas_per_sm = occ.get();
     const int n_tiles = L.n_qt * L.B * L.Hq;
     const int grid = n_tiles < sms * ctas_per_sm ? n_tiles : sms * ctas_per_sm;
     quantize_q_kernel<T, D><<<grid, 256, q_smem, st>>>(qv, L.Hq, L.N, L.Nq_pad, L.n_qt, n_tiles, L.qmax, L.means, Ht,
@@ -791,11 +790,11 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
   }
   dim3 gk(L.n_kb, L.B * L.Hkv);
   constexpr int kv_smem = kv_smem_bytes<T, D>();
-  static bool attr_set = false;  // per template instance; benign race (idempotent)
-  if (!attr_set && kv_smem > 48 * 1024) {
-    cudaFuncSetAttribute(quantize_kv_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kv_smem);
-  }
-  attr_set = true;
+  static PerDevice kv_once;
+  cudaError_t e = kv_once.run([&](std::atomic<int>&) {
+    return cudaFuncSetAttribute(quantize_kv_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kv_smem);
+  });
+  if (e != cudaSuccess) return e;
   quantize_kv_kernel<T, D><<<gk, 256, kv_smem, st>>>(kv, vv, L.Hq, L.Hkv, L.N, L.Np, L.n_kb, L.qmax, L.v_r, L.smoothing,
                                                L.sm_scale_log2, L.means, Ht, L.k_codes, L.v_codes, L.kv_meta,
                                                L.kv_scale64, L.bias, L.bias_l2);

@@ -50,10 +50,10 @@ Dims dims_of(const sa2pp_problem& p) {
   return d;
 }
 
-constexpr int kRowsPerChunk = 512;
-
+// NaN selects the reference default 1/sqrt(head_dim) (attention.py:87-91); any finite value,
+// zero and negative included, is used as given, as AttentionConfig.softmax_scale is.
 double sm_scale_of(const sa2pp_problem& p) {
-  return p.sm_scale > 0.0 ? p.sm_scale : 1.0 / std::sqrt(static_cast<double>(p.head_dim));
+  return std::isnan(p.sm_scale) ? 1.0 / std::sqrt(static_cast<double>(p.head_dim)) : p.sm_scale;
 }
 
 bool aligned16(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; }
@@ -100,6 +100,7 @@ int sa2pp_check_problem(const sa2pp_problem* p) {
   if (p->buffering_depth != 1 && p->buffering_depth != 2)
     return fail(SA2PP_ERR_RANGE, "buffering_depth must be 1 or 2, got %d", p->buffering_depth);
   if (!(p->p_r > 0.0) || !(p->v_r > 0.0)) return fail(SA2PP_ERR_RANGE, "p_r and v_r must be positive");
+  if (std::isinf(p->sm_scale)) return fail(SA2PP_ERR_INVALID, "sm_scale must be finite (NaN selects 1/sqrt(D))");
   const double bound = kRangeProductLimit / p->buffering_depth;
   if (!p->expect_overflow && p->p_r * p->v_r > bound)
     return fail(SA2PP_ERR_RANGE, "p_r*v_r = %g > %g (FP16 accumulator bound at buffering depth %d)",
@@ -129,8 +130,7 @@ int sa2pp_quant_sizes(const sa2pp_problem* p, sa2pp_quant_sizes_t* s) {
   s->bias = B * Hq * d.np * 4;
   s->bias_l2 = B * Hq * d.np * 4;
   s->means = B * (Hq + Hkv) * D * 8;
-  const int64_t chunks = (p->seq_len + kRowsPerChunk - 1) / kRowsPerChunk;
-  s->workspace = B * (Hq + Hkv) * chunks * D * 16;
+  s->workspace = 0;  // reserved: the current kernels need no scratch
   return SA2PP_OK;
 }
 
@@ -169,8 +169,7 @@ int sa2pp_prepass(const sa2pp_problem* p, const sa2pp_inputs* in, const sa2pp_qu
     return rc;
   sa2pp_quant_sizes_t sz;
   sa2pp_quant_sizes(p, &sz);
-  if (p->smoothing && (ws == nullptr || ws_bytes < sz.workspace))
-    return fail(SA2PP_ERR_INVALID, "workspace too small: need %zu bytes", sz.workspace);
+  if (ws_bytes < sz.workspace) return fail(SA2PP_ERR_INVALID, "workspace too small: need %zu bytes", sz.workspace);
   const Dims d = dims_of(*p);
   sa2pp::PrepassLaunch L{};
   L.dtype = in->dtype;
@@ -185,8 +184,6 @@ int sa2pp_prepass(const sa2pp_problem* p, const sa2pp_inputs* in, const sa2pp_qu
   L.n_kb = static_cast<int>(d.n_kb);
   L.qmax = (1 << (p->qk_bits - 1)) - 1;
   L.smoothing = p->smoothing ? 1 : 0;
-  L.rows_per_chunk = kRowsPerChunk;
-  L.n_chunks = static_cast<int>((p->seq_len + kRowsPerChunk - 1) / kRowsPerChunk);
   L.v_r = p->v_r;
   L.sm_scale_log2 = sm_scale_of(*p) * 1.4426950408889634;
   L.q = in->q;
@@ -197,7 +194,6 @@ int sa2pp_prepass(const sa2pp_problem* p, const sa2pp_inputs* in, const sa2pp_qu
     L.k_stride[i] = in->k_stride[i];
     L.v_stride[i] = in->v_stride[i];
   }
-  L.partial = static_cast<double2*>(ws);
   L.means = qt->means;
   L.q_codes = qt->q_codes;
   L.q_scale = qt->q_scale;

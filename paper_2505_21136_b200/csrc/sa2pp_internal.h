@@ -1,6 +1,7 @@
 // Internal launch descriptors shared by the C-ABI layer and the kernels.
 #pragma once
 #include <cuda_runtime.h>
+#include <atomic>
 #include <cstdint>
 
 #include "../../include/sa2pp.h"
@@ -13,13 +14,35 @@ constexpr int kBlockK = 64;   // attention.py:63
 // Record the calling thread's last error (sa2pp_last_error) and return `code`.
 int set_error(int code, const char* fmt, ...);
 
+// One-time per-device setup (cudaFuncSetAttribute and occupancy queries apply to one device's
+// context): `run(f)` calls f once per device ordinal and caches success; concurrent first calls may
+// both run f, which is idempotent.
+struct PerDevice {
+  std::atomic<uint64_t> done{0};
+  std::atomic<int> value[64] = {};
+  template <class F>
+  cudaError_t run(F&& f) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = f(value[dev & 63]);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
+    return e;
+  }
+  int get() const {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return value[dev & 63].load(std::memory_order_relaxed);
+  }
+};
+
 struct PrepassLaunch {
   int dtype, D, B, Hq, Hkv, N, Nq_pad, Np, n_qt, n_kb, qmax, smoothing;
-  int rows_per_chunk, n_chunks;
   double v_r, sm_scale_log2;
   const void *q, *k, *v;
   int64_t q_stride[3], k_stride[3], v_stride[3];
-  double2* partial;
   double* means;
   int8_t* q_codes;
   float* q_scale;
