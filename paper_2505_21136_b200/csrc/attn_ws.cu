@@ -1,0 +1,533 @@
+// SageAttention2++ forward on sm_100a, warp-specialised: INT8 QK^T and FP8 PV on tcgen05 tensor cores.
+//
+// One CTA (256 threads, two CTAs resident per SM) owns one 128-row query tile of one (batch, head) and
+// walks the 64-key blocks in ascending order, which is part of the reference's numerical contract
+// (lpattn attention.py:6-8).  Two warpgroups, one query row per thread in each:
+//
+//   softmax warps 0-3 (thread = row r, all 64 score columns of the block)
+//     tcgen05.ld S -> t = S*(dQ dK sm_scale log2e) + bias_j*sm_scale log2e, causal/pad mask
+//     (attention.py:285-294); row max in-thread; online softmax with l from the unquantized P~
+//     (attention.py:136-154); the tile-wide P scale (quantization.py:163-175: dP = max|P~|/p_r over
+//     128x64) from the four warps' max-shifts through a split-phase mbarrier (publish after the row
+//     max, wait after the exponentials); P^ = E4M3(P~/dP) into TMEM over the S columns it read;
+//     alpha_j (per row) and dP_j published for the promotion.
+//   promotion warps 4-7 (thread = row r, all D output channels, O in registers)
+//     O = O*alpha_j + pv_j*(dP_j*dV_j[c]) with pv_j the FP16 (or FP32) PV accumulator of block j
+//     (mma.py:144-166, attention.py:303); at the end O / l (attention.py:304-305).
+//     Warp 4 also issues, from one elected lane, once the softmax warps finished block j and the
+//     promotion warps drained PV(j-1):
+//       PV(j)   = P^(j).V^_j   kind::f8f6f4, A = P^ from TMEM, B = V^T from smem, M=128 N=D, two
+//                              k=32 MMAs (the reference's depth-2 grouping), F16 or F32 accumulator
+//       S(j+2)  = Q^.K^_(j+2)^T kind::i8, M=128 N=64 K=D, S32 into S[j&1] (after PV(j) read P^(j):
+//                              tcgen05 MMAs from one thread execute in order)
+//       TMA     refill of the stage block j-1 used (its last readers were PV(j-1) and its promotion).
+//
+// The softmax warps never wait for the promotion and vice versa except through the single PV
+// accumulator, so block j's promotion overlaps block j+1's softmax.  Registers: setmaxnreg moves
+// them from the softmax warpgroup (64 score registers) to the promotion warpgroup (D accumulators).
+//
+// TMEM (256 columns per CTA): S[0] [0,64), S[1] [64,128), PV [128, 128+D).  P^ of block j (E4M3, four
+// keys per column) is written over S[j&1] columns [0,16) of the same lane.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda.h>
+#include <cstdint>
+#include <type_traits>
+
+#include "ptx.cuh"
+#include "sa2pp_internal.h"
+
+namespace sa2pp {
+
+template <int D>
+struct WsCfg {
+  static constexpr int kStages = (D == 128) ? 4 : 8;  // powers of two: stage/parity math is masks
+  static constexpr int kQBytes = 128 * D;
+  static constexpr int kKBytes = 64 * D;
+  static constexpr int kVBytes = D * 64;
+  static constexpr int kMetaBytes = (4 + D) * 4;
+  static constexpr int kBiasBytes = 64 * 4;
+  static constexpr uint32_t kLayoutQK = (D == 128) ? 2u : 4u;  // SWIZZLE_128B / SWIZZLE_64B
+  static constexpr uint32_t kSboQK = 8 * D;                     // bytes between 8-row core groups
+  static constexpr uint32_t kLayoutV = 4u;                      // V^T rows are 64 keys = 64 B
+  static constexpr uint32_t kSboV = 512;
+  static constexpr int kTmemCols = 256;
+  static constexpr int kColPV = 128;
+  // shared memory carve-up (offsets from a 1024-aligned base)
+  static constexpr int kOffQ = 0;
+  static constexpr int kOffK = kOffQ + kQBytes;
+  static constexpr int kOffV = kOffK + kStages * kKBytes;
+  static constexpr int kOffMeta = kOffV + kStages * kVBytes;
+  static constexpr int kOffBias = kOffMeta + kStages * kMetaBytes;
+  static constexpr int kOffF = kOffBias + kStages * kBiasBytes;  // [4 promotion warps][D] dP_j*dV_j[c]
+  static constexpr int kOffAlpha = kOffF + 4 * D * 4;             // [4][128] alpha_j per row (j & 3)
+  static constexpr int kOffDp = kOffAlpha + 4 * 128 * 4;          // [4] dP_j (j & 3)
+  static constexpr int kOffRed = kOffDp + 4 * 4;                  // [2][4] per-warp max-shift candidates
+  static constexpr int kOffL = kOffRed + 2 * 4 * 4;               // [128] final row sums
+  static constexpr int kOffBar = kOffL + 128 * 4;
+  static constexpr int kNumBars = 1 + kStages + 2 + 2 + 1 + 1 + 2 + 1;
+  static constexpr int kOffTmem = kOffBar + kNumBars * 8;
+  static constexpr int kSmemBytes = kOffTmem + 16 + 1024;  // + alignment slack
+  static constexpr int kThreads = 256;
+  // register split (setmaxnreg): the launch gives 128 per thread
+  static constexpr uint32_t kRegSoftmax = (D == 128) ? 88 : 128;
+  static constexpr uint32_t kRegPromote = (D == 128) ? 168 : 128;
+  static_assert(kRegSoftmax + kRegPromote == 256, "the two warpgroups share the launch budget");
+  static_assert(2 * kSmemBytes <= 227 * 1024, "two CTAs per SM must fit in shared memory");
+  static_assert((kStages & (kStages - 1)) == 0, "stage count must be a power of two");
+};
+
+template <int N, typename OutT>
+__device__ __forceinline__ void store_row(OutT* dst, const float2 (&O)[N / 2], float inv_l) {
+  if constexpr (sizeof(OutT) == 4) {
+#pragma unroll
+    for (int c = 0; c < N / 2; c += 2) {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + 2 * c) =
+          make_float4(O[c].x * inv_l, O[c].y * inv_l, O[c + 1].x * inv_l, O[c + 1].y * inv_l);
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < N / 2; c += 4) {
+      uint32_t w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float a = O[c + i].x * inv_l, b = O[c + i].y * inv_l;
+        if constexpr (std::is_same<OutT, __nv_bfloat16>::value) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+          w[i] = *reinterpret_cast<uint32_t*>(&h);
+        } else {
+          __half2 h = __floats2half2_rn(a, b);
+          w[i] = *reinterpret_cast<uint32_t*>(&h);
+        }
+      }
+      *reinterpret_cast<uint4*>(dst + 2 * c) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+  }
+}
+
+template <int D, bool CAUSAL, bool ACC16, bool INSTR, typename OutT>
+__global__ void __launch_bounds__(256, 2)
+    attn_ws_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                   const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
+  using C = WsCfg<D>;
+  constexpr int S = C::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  // ---- work decode: grid = (n_qt, B*Hq); causal runs the heaviest query tiles first
+  const int bh = blockIdx.y;
+  const int b = bh / p.Hq;
+  const int hq = bh % p.Hq;
+  const int hkv = hq / p.group;
+  const int qt = CAUSAL ? (p.n_qt - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
+  const int q0 = qt * 128;
+  const int nblk = CAUSAL ? min(p.n_kb, (min(q0 + 128, p.N) + 63) / 64) : p.n_kb;
+
+  uint64_t* bar_base = reinterpret_cast<uint64_t*>(smem + C::kOffBar);
+  uint64_t* q_full = bar_base;
+  uint64_t* kv_full = q_full + 1;    // [S] TMA landed
+  uint64_t* s_full = kv_full + S;    // [2] S(j) in TMEM
+  uint64_t* p_ready = s_full + 2;    // [2] the 4 softmax warps stored P^(j) and published alpha_j, dP_j
+  uint64_t* pv_full = p_ready + 2;   // [1] PV(j) in TMEM
+  uint64_t* pv_free = pv_full + 1;   // [1] the 4 promotion warps drained PV(j)
+  uint64_t* dt_bar = pv_free + 1;    // [2] the 4 softmax warps published their max-shift
+  uint64_t* l_ready = dt_bar + 2;    // [1] final row sums written
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
+  float* alpha_s = reinterpret_cast<float*>(smem + C::kOffAlpha);
+  float* dp_s = reinterpret_cast<float*>(smem + C::kOffDp);
+  float* red = reinterpret_cast<float*>(smem + C::kOffRed);
+  float* lbuf = reinterpret_cast<float*>(smem + C::kOffL);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_init(q_full, 1);
+      for (int s = 0; s < S; ++s) mbar_init(&kv_full[s], 1);
+      for (int x = 0; x < 2; ++x) {
+        mbar_init(&s_full[x], 1);
+        mbar_init(&p_ready[x], 4);
+        mbar_init(&dt_bar[x], 4);
+      }
+      mbar_init(pv_full, 1);
+      mbar_init(pv_free, 4);
+      mbar_init(l_ready, 4);
+      fence_barrier_init();
+    }
+    __syncwarp();
+    tmem_alloc(tmem_holder, C::kTmemCols);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const int wq = warp & 3;       // TMEM lane quarter of this warp
+  const int r = wq * 32 + lane;  // query row within the tile
+  const uint32_t tm_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
+  const int row_g = q0 + r;
+  const bool row_valid = row_g < p.N;
+
+  if (warp < 4) {
+    // =============================== softmax warpgroup ===============================
+    if constexpr (C::kRegSoftmax < 128) setmaxnreg_dec<C::kRegSoftmax>();
+    const float a_q = p.q_scale[static_cast<int64_t>(bh) * p.n_qt + qt] * p.sm_scale_log2;
+    const bool dbg = INSTR && (p.debug != nullptr) && qt == 0 && bh == 0;
+    float m_run = -INFINITY, l_run = 0.0f;
+
+    // One key block.  MASK: causal diagonal / padded-tail block (attention.py:128-133, 293-294).
+    auto block = [&](int j, auto mask_tag) {
+      constexpr bool MASK = decltype(mask_tag)::value;
+      const int P = j & 1;
+      const int st = static_cast<int>(static_cast<unsigned>(j) % S);
+      mbar_wait_sleep(&kv_full[st], (static_cast<unsigned>(j) / S) & 1);  // bias / dK of this stage
+      mbar_wait_sleep(&s_full[P], (j >> 1) & 1);
+      tc_fence_after();
+      const float* meta = reinterpret_cast<const float*>(smem + C::kOffMeta + st * C::kMetaBytes);
+      const float* cb = reinterpret_cast<const float*>(smem + C::kOffBias + st * C::kBiasBytes);
+      const uint32_t s_addr = tm_row + P * 64;
+      const float a = a_q * ld_shared_f32(meta);
+      const float2 a2 = make_float2(a, a);
+      // ---- t = S_int * (dQ dK sm_scale log2e) + bias_j * sm_scale log2e  (attention.py:287-292),
+      //      causal / pad mask, row max.  Half 0 (keys 0-31) goes back into TMEM over its S columns,
+      //      half 1 stays in registers.
+      auto scores = [&](int hlf, float2 (&x)[16]) {
+        uint32_t sr[32];
+        tmem_ld32(s_addr + hlf * 32, sr);
+        tmem_wait_ld();
+        if constexpr (INSTR) {
+          if (dbg && j == 0) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) p.debug[r * 64 + hlf * 32 + i] = sr[i];
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const float4 c4 = ld_shared_f4(cb + hlf * 32 + 2 * i);
+          x[i] = __ffma2_rn(make_float2(static_cast<float>(static_cast<int>(sr[2 * i])),
+                                        static_cast<float>(static_cast<int>(sr[2 * i + 1]))),
+                            a2, make_float2(c4.x, c4.y));
+          x[i + 1] = __ffma2_rn(make_float2(static_cast<float>(static_cast<int>(sr[2 * i + 2])),
+                                            static_cast<float>(static_cast<int>(sr[2 * i + 3]))),
+                                a2, make_float2(c4.z, c4.w));
+        }
+        if constexpr (MASK) {
+          const int lim = CAUSAL ? min(row_g + 1, p.N) : p.N;  // keys >= lim are masked
+          const int key0 = j * 64 + hlf * 32;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            if (key0 + 2 * i >= lim) x[i].x = -INFINITY;
+            if (key0 + 2 * i + 1 >= lim) x[i].y = -INFINITY;
+          }
+        }
+        float m4[4];  // four independent max chains, then combine
+#pragma unroll
+        for (int q4 = 0; q4 < 4; ++q4) {
+          m4[q4] = fmax3(x[4 * q4].x, x[4 * q4].y, x[4 * q4 + 1].x);
+          m4[q4] = fmax3(m4[q4], x[4 * q4 + 1].y, x[4 * q4 + 2].x);
+          m4[q4] = fmax3(m4[q4], x[4 * q4 + 2].y, x[4 * q4 + 3].x);
+          m4[q4] = fmaxf(m4[q4], x[4 * q4 + 3].y);
+        }
+        return fmaxf(fmax3(m4[0], m4[1], m4[2]), m4[3]);
+      };
+      float2 x[16];
+      float rmax = scores(0, x);
+      tmem_st32(s_addr, reinterpret_cast<const uint32_t(&)[32]>(x));
+      rmax = fmaxf(rmax, scores(1, x));
+      const float m_new = fmaxf(m_run, rmax);
+      // ---- tile-max candidate: rowmax - m_new = min(0, rowmax - m_old); each warp publishes the
+      //      min over its rows of -that (>= 0; +inf for rows that do not count) as float bits
+      {
+        const float v = (row_valid && rmax != -INFINITY) ? fmaxf(0.0f, m_run - rmax) : INFINITY;
+        const uint32_t vmin = __reduce_min_sync(0xffffffffu, __float_as_uint(v));
+        if (lane == 0) {
+          red[P * 4 + wq] = __uint_as_float(vmin);
+          mbar_arrive(&dt_bar[P]);  // release: the store above is visible to every waiter
+        }
+      }
+      const float alpha = (m_new == -INFINITY) ? 1.0f : ex2(m_run - m_new);
+      // ---- tile scale (quantization.py:163-175): dP = max P~ / p_r = 2^Dt / p_r with
+      //      Dt = max over the tile of (rowmax - m_new) <= 0, so P^ = P~ / dP = exp2(t - m_new + log2 p_r - Dt)
+      //      in one exponential; l accumulates the unquantized P~ = P^ * dP (attention.py:149-153)
+      mbar_wait(&dt_bar[P], (j >> 1) & 1);
+      const float4 rv = ld_shared_f4(red + P * 4);
+      float sh = fminf(fminf(rv.x, rv.y), fminf(rv.z, rv.w));  // -Dt >= 0
+      sh = (sh == INFINITY) ? 0.0f : sh;
+      const float dP = ex2(-sh) * p.inv_pr;
+      if (INSTR && p.report != nullptr && threadIdx.x == 0) {
+        atomicMin(&p.report->p_scale_min_bits, __float_as_uint(dP));
+        atomicMax(&p.report->p_scale_max_bits, __float_as_uint(dP));
+      }
+      const float m_eff = (m_new == -INFINITY) ? 0.0f : (m_new - p.log2_pr - sh);
+      const float2 nme2 = make_float2(-m_eff, -m_eff);
+      uint32_t pk[16];
+      float2 rs[4] = {make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f), make_float2(0.0f, 0.0f),
+                      make_float2(0.0f, 0.0f)};
+      auto quant = [&](const float2 (&t)[16], int w0) {  // P^ codes of 32 keys into pk[w0, w0+8)
+#pragma unroll
+        for (int i = 0; i < 16; i += 2) {
+          const float2 u0 = __fadd2_rn(t[i], nme2), u1 = __fadd2_rn(t[i + 1], nme2);
+          const float2 e0 = make_float2(ex2(u0.x), ex2(u0.y)), e1 = make_float2(ex2(u1.x), ex2(u1.y));
+          rs[(i >> 1) & 3] = __fadd2_rn(rs[(i >> 1) & 3], __fadd2_rn(e0, e1));
+          pk[w0 + i / 2] = pack_e4m3x2(e0.x, e0.y) | (pack_e4m3x2(e1.x, e1.y) << 16);
+        }
+      };
+      quant(x, 8);  // keys 32-63 (registers)
+      {
+        tmem_wait_st();
+        uint32_t tr[32];
+        tmem_ld32(s_addr, tr);  // keys 0-31 (t stored above)
+        tmem_wait_ld();
+        quant(reinterpret_cast<const float2(&)[16]>(tr), 0);
+      }
+      const float2 r2 = __fadd2_rn(__fadd2_rn(rs[0], rs[1]), __fadd2_rn(rs[2], rs[3]));
+      l_run = l_run * alpha + (r2.x + r2.y) * dP;
+      tmem_st16(s_addr, pk);
+      alpha_s[(j & 3) * 128 + r] = alpha;
+      if (threadIdx.x == 0) dp_s[j & 3] = dP;
+      tmem_wait_st();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&p_ready[P]);  // release: alpha/dP stores and P^ in TMEM
+      m_run = m_new;
+    };
+
+    // Blocks entirely below the causal diagonal and inside the sequence need no mask.
+    const int n_plain = CAUSAL ? min(nblk, q0 / 64) : ((p.N % 64 == 0) ? nblk : nblk - 1);
+    int j = 0;
+    for (; j < n_plain; ++j) block(j, std::false_type{});
+    for (; j < nblk; ++j) block(j, std::true_type{});
+    lbuf[r] = l_run;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(l_ready);
+  } else {
+    // =============================== promotion warpgroup (+ issue) ===============================
+    if constexpr (C::kRegPromote > 128) setmaxnreg_inc<C::kRegPromote>();
+    const int kv_row = (b * p.Hkv + hkv) * p.Np;
+    const int vt_row = (b * p.Hkv + hkv) * D;
+    const float* meta_src = p.kv_meta + static_cast<int64_t>(b * p.Hkv + hkv) * p.n_kb * (4 + D);
+    const float* bias_src = p.bias_l2 + static_cast<int64_t>(bh) * p.Np;
+    constexpr uint32_t idesc_qk = make_idesc(2u, 1u, 1u, 128u, 64u);             // S32 <- s8 x s8
+    constexpr uint32_t idesc_pv = make_idesc(ACC16 ? 0u : 1u, 0u, 0u, 128u, D);  // F16|F32 <- e4m3 x e4m3
+    auto load_block = [&](int j) {  // one thread
+      const int st = static_cast<int>(static_cast<unsigned>(j) % S);
+      mbar_arrive_expect_tx(&kv_full[st], C::kKBytes + C::kVBytes + C::kMetaBytes + C::kBiasBytes);
+      tma_load_2d(smem + C::kOffK + st * C::kKBytes, &tm_k, &kv_full[st], 0, kv_row + j * 64);
+      tma_load_2d(smem + C::kOffV + st * C::kVBytes, &tm_v, &kv_full[st], j * 64, vt_row);
+      bulk_load(smem + C::kOffMeta + st * C::kMetaBytes, meta_src + static_cast<int64_t>(j) * (4 + D), C::kMetaBytes,
+                &kv_full[st]);
+      bulk_load(smem + C::kOffBias + st * C::kBiasBytes, bias_src + j * 64, C::kBiasBytes, &kv_full[st]);
+    };
+    auto issue_qk = [&](int j) {  // one thread; K^_j must have landed
+      const int st = static_cast<int>(static_cast<unsigned>(j) % S);
+      const uint64_t qdesc = smem_desc(smem_u32(smem + C::kOffQ), C::kSboQK, C::kLayoutQK);
+      const uint64_t kdesc = smem_desc(smem_u32(smem + C::kOffK + st * C::kKBytes), C::kSboQK, C::kLayoutQK);
+      const uint32_t d_tm = tmem + (j & 1) * 64;
+#pragma unroll
+      for (int kk = 0; kk < D / 32; ++kk) umma_i8_ss(d_tm, qdesc + 2 * kk, kdesc + 2 * kk, idesc_qk, kk > 0 ? 1u : 0u);
+      umma_commit(&s_full[j & 1]);
+    };
+    auto issue_pv = [&](int j) {  // one thread; P^(j) stored, PV(j-1) drained
+      const int st = static_cast<int>(static_cast<unsigned>(j) % S);
+      const uint64_t vdesc = smem_desc(smem_u32(smem + C::kOffV + st * C::kVBytes), C::kSboV, C::kLayoutV);
+      const uint32_t a_tm = tmem + (j & 1) * 64;
+      umma_f8_ts(tmem + C::kColPV, a_tm, vdesc, idesc_pv, 0u);           // keys  0..31: P^ cols [0,8)
+      umma_f8_ts(tmem + C::kColPV, a_tm + 8, vdesc + 2, idesc_pv, 1u);   // keys 32..63: P^ cols [8,16)
+      umma_commit(pv_full);
+    };
+    if (warp == 4 && elect_one()) {
+      tma_prefetch_desc(&tm_q);
+      tma_prefetch_desc(&tm_k);
+      tma_prefetch_desc(&tm_v);
+      mbar_arrive_expect_tx(q_full, C::kQBytes);
+      tma_load_2d(smem + C::kOffQ, &tm_q, q_full, 0, bh * p.Nq_pad + q0);
+      for (int j = 0; j < min(S, nblk); ++j) load_block(j);
+      mbar_wait(q_full, 0);
+      mbar_wait(&kv_full[0], 0);
+      issue_qk(0);
+      if (nblk > 1) {
+        mbar_wait(&kv_full[1], 0);
+        issue_qk(1);
+      }
+    }
+    __syncwarp();
+
+    const int pw = warp - 4;  // promotion warp index = TMEM lane quarter
+    float* fw = reinterpret_cast<float*>(smem + C::kOffF) + pw * D;
+    const bool dbg = INSTR && (p.debug != nullptr) && qt == 0 && bh == 0;
+    const bool want_overflow = INSTR && ACC16 && p.report != nullptr;
+    uint32_t overflow = 0;
+    float2 O[D / 2];
+#pragma unroll
+    for (int c = 0; c < D / 2; ++c) O[c] = make_float2(0.0f, 0.0f);
+
+    // O[c] = O[c]*alpha + pv[c]*f[c] for the row's D channels (attention.py:303).
+    auto promote_impl = [&](int j, float alpha, auto resc_tag) {
+      constexpr bool RESC = decltype(resc_tag)::value;
+      const float2 al2 = make_float2(alpha, alpha);
+      constexpr int CH = ACC16 ? 32 : 16;  // channels per TMEM load (16 registers either way)
+#pragma unroll
+      for (int c0 = 0; c0 < D; c0 += CH) {
+        float2 pv[CH / 2];
+        if constexpr (ACC16) {
+          uint32_t v[CH / 2];
+          tmem_ld16_pack16(tm_row + C::kColPV + c0, v);  // F16 accumulators, 2 per register
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < CH / 2; ++i) pv[i] = f16x2_to_f32x2(v[i]);
+          if (want_overflow) {
+#pragma unroll
+            for (int i = 0; i < CH / 2; ++i)
+              overflow += ((v[i] & 0x7C00u) == 0x7C00u) + ((v[i] & 0x7C000000u) == 0x7C000000u);
+          }
+        } else {
+          uint32_t v[CH];
+          tmem_ld16(tm_row + C::kColPV + c0, v);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < CH / 2; ++i) pv[i] = make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+        }
+        if constexpr (INSTR) {
+          if (dbg && j == 0) {
+#pragma unroll
+            for (int i = 0; i < CH / 2; ++i) {
+              p.debug[128 * 64 + r * D + c0 + 2 * i] = __float_as_uint(pv[i].x);
+              p.debug[128 * 64 + r * D + c0 + 2 * i + 1] = __float_as_uint(pv[i].y);
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < CH / 2; i += 2) {
+          const float4 fv = ld_shared_f4(fw + c0 + 2 * i);
+          if constexpr (RESC) {
+            O[c0 / 2 + i] = __ffma2_rn(pv[i], make_float2(fv.x, fv.y), __fmul2_rn(O[c0 / 2 + i], al2));
+            O[c0 / 2 + i + 1] = __ffma2_rn(pv[i + 1], make_float2(fv.z, fv.w), __fmul2_rn(O[c0 / 2 + i + 1], al2));
+          } else {
+            O[c0 / 2 + i] = __ffma2_rn(pv[i], make_float2(fv.x, fv.y), O[c0 / 2 + i]);
+            O[c0 / 2 + i + 1] = __ffma2_rn(pv[i + 1], make_float2(fv.z, fv.w), O[c0 / 2 + i + 1]);
+          }
+        }
+        if constexpr (CH == 32) {
+          reg_fence32(reinterpret_cast<float*>(&O[c0 / 2]));
+        } else {
+          reg_fence16(reinterpret_cast<float*>(&O[c0 / 2]));
+        }
+      }
+    };
+
+    for (int j = 0; j < nblk; ++j) {
+      const int st = static_cast<int>(static_cast<unsigned>(j) % S);
+      if (warp == 4) {  // ---- issue PV(j), S(j+2) and the refill of block j-1's stage
+        mbar_wait_sleep(&p_ready[j & 1], (j >> 1) & 1);
+        if (j > 0) mbar_wait(pv_free, (j - 1) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          issue_pv(j);
+          if (j + 2 < nblk) {
+            mbar_wait(&kv_full[static_cast<unsigned>(j + 2) % S], (static_cast<unsigned>(j + 2) / S) & 1);
+            issue_qk(j + 2);
+          }
+          if (j >= 1 && j - 1 + S < nblk) load_block(j - 1 + S);
+        }
+        __syncwarp();
+      }
+      // ---- promotion of block j: f[c] = dP_j * dV_j[c] for this warp's copy
+      mbar_wait_sleep(&kv_full[st], (static_cast<unsigned>(j) / S) & 1);  // dV of this stage visible
+      mbar_wait_sleep(pv_full, static_cast<uint32_t>(j) & 1u);
+      tc_fence_after();
+      const float dP = dp_s[j & 3];
+      const float alpha = alpha_s[(j & 3) * 128 + r];
+      {
+        const float* meta = reinterpret_cast<const float*>(smem + C::kOffMeta + st * C::kMetaBytes);
+#pragma unroll
+        for (int c = 4 * lane; c < D; c += 128) {
+          const float4 dv = ld_shared_f4(meta + 4 + c);
+          *reinterpret_cast<float4*>(fw + c) = make_float4(dP * dv.x, dP * dv.y, dP * dv.z, dP * dv.w);
+        }
+      }
+      __syncwarp();
+      if (__any_sync(0xffffffffu, alpha != 1.0f)) {
+        promote_impl(j, alpha, std::true_type{});
+      } else {
+        promote_impl(j, alpha, std::false_type{});
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(pv_free);
+    }
+    if (want_overflow && overflow) atomicAdd(&p.report->overflow_events, overflow);
+    // ---- O / l (attention.py:304-305)
+    mbar_wait_sleep(l_ready, 0);
+    if (row_valid) {
+      const float l = lbuf[r];
+      const float inv_l = 1.0f / (l == 0.0f ? 1.0f : l);
+      OutT* dst = reinterpret_cast<OutT*>(p.out) + b * p.o_sb + hq * p.o_sh + static_cast<int64_t>(row_g) * p.o_sn;
+      store_row<D, OutT>(dst, O, inv_l);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, C::kTmemCols);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+template <int D, bool CAUSAL, bool ACC16, bool INSTR, typename OutT>
+static cudaError_t launch_ws_t(const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
+  using C = WsCfg<D>;
+  CUtensorMap mq, mk, mv;
+  const CUtensorMapSwizzle swqk = (D == 128) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  if (!make_map_2d(&mq, qt.q_codes, D, static_cast<uint64_t>(P.B) * P.Hq * P.Nq_pad, D, D, 128, swqk) ||
+      !make_map_2d(&mk, qt.k_codes, D, static_cast<uint64_t>(P.B) * P.Hkv * P.Np, D, D, 64, swqk) ||
+      !make_map_2d(&mv, qt.v_codes, P.Np, static_cast<uint64_t>(P.B) * P.Hkv * D, P.Np, 64, D,
+                   CU_TENSOR_MAP_SWIZZLE_64B))
+    return cudaErrorInvalidValue;
+  auto kern = attn_ws_kernel<D, CAUSAL, ACC16, INSTR, OutT>;
+  static PerDevice once;
+  cudaError_t e = once.run([&](std::atomic<int>&) {
+    cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (r == cudaSuccess) r = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    return r;
+  });
+  if (e != cudaSuccess) return e;
+  dim3 grid(P.n_qt, P.B * P.Hq);
+  kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(mq, mk, mv, P);
+  return cudaGetLastError();
+}
+
+template <int D, bool CAUSAL, bool ACC16, bool INSTR>
+static cudaError_t launch_ws_outi(const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
+  switch (P.out_dtype) {
+    case SA2PP_F32: return launch_ws_t<D, CAUSAL, ACC16, INSTR, float>(P, qt, st);
+    case SA2PP_F16: return launch_ws_t<D, CAUSAL, ACC16, INSTR, __half>(P, qt, st);
+    case SA2PP_BF16: return launch_ws_t<D, CAUSAL, ACC16, INSTR, __nv_bfloat16>(P, qt, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int D, bool CAUSAL, bool ACC16>
+static cudaError_t launch_ws_out(const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
+  if (P.debug != nullptr || P.report != nullptr) return launch_ws_outi<D, CAUSAL, ACC16, true>(P, qt, st);
+  return launch_ws_outi<D, CAUSAL, ACC16, false>(P, qt, st);
+}
+
+template <int D>
+static cudaError_t launch_ws_d(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt,
+                               cudaStream_t st) {
+  const bool acc16 = prob.pv_accum == SA2PP_ACC_F16;
+  if (prob.causal) {
+    return acc16 ? launch_ws_out<D, true, true>(P, qt, st) : launch_ws_out<D, true, false>(P, qt, st);
+  }
+  return acc16 ? launch_ws_out<D, false, true>(P, qt, st) : launch_ws_out<D, false, false>(P, qt, st);
+}
+
+cudaError_t launch_attn_ws(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
+  if (prob.head_dim == 128) return launch_ws_d<128>(prob, P, qt, st);
+  if (prob.head_dim == 64) return launch_ws_d<64>(prob, P, qt, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace sa2pp

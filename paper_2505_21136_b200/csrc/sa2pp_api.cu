@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdarg>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -243,7 +244,12 @@ int sa2pp_attn_fwd(const sa2pp_problem* p, const sa2pp_quant* qt, const sa2pp_ou
   P.report = report;
   P.debug = g_debug;
   P.trace = g_trace;
-  cudaError_t e = sa2pp::launch_attn(*p, P, *qt, static_cast<cudaStream_t>(stream));
+  static const bool use_v4 = [] {
+    const char* v = std::getenv("SA2PP_ATTN");
+    return v != nullptr && std::strcmp(v, "v4") == 0;
+  }();
+  cudaError_t e = use_v4 || P.trace != nullptr ? sa2pp::launch_attn(*p, P, *qt, static_cast<cudaStream_t>(stream))
+                                                : sa2pp::launch_attn_ws(*p, P, *qt, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return SA2PP_OK;
 }
