@@ -11,6 +11,8 @@ import os
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libsa2pp.so"
+if os.environ.get("SA2PP_LIB"):  # development A/B of library builds (tools/build_variant.py)
+    LIB_PATH = Path(os.environ["SA2PP_LIB"]).resolve()
 
 SA2PP_OK, SA2PP_ERR_INVALID, SA2PP_ERR_UNSUPPORTED, SA2PP_ERR_RANGE, SA2PP_ERR_CUDA = range(5)
 SA2PP_F32, SA2PP_F16, SA2PP_BF16 = range(3)

@@ -37,11 +37,31 @@
 #include "ptx.cuh"
 #include "sa2pp_internal.h"
 
+// Tuning knobs (overridable with -D for A/B builds, tools/build_variant.py)
+#ifndef SA2PP_WS_REG_SOFTMAX
+#define SA2PP_WS_REG_SOFTMAX 88
+#endif
+#ifndef SA2PP_WS_PV_CHUNK
+#define SA2PP_WS_PV_CHUNK 32
+#endif
+#ifndef SA2PP_WS_F_PREFETCH
+#define SA2PP_WS_F_PREFETCH 0
+#endif
+#ifndef SA2PP_WS_FANOUT
+#define SA2PP_WS_FANOUT 0
+#endif
+#ifndef SA2PP_WS_PIPE
+#define SA2PP_WS_PIPE 1
+#endif
+#ifndef SA2PP_WS_STAGES128
+#define SA2PP_WS_STAGES128 4
+#endif
+
 namespace sa2pp {
 
 template <int D>
 struct WsCfg {
-  static constexpr int kStages = (D == 128) ? 4 : 8;  // powers of two: stage/parity math is masks
+  static constexpr int kStages = (D == 128) ? SA2PP_WS_STAGES128 : 8;
   static constexpr int kQBytes = 128 * D;
   static constexpr int kKBytes = 64 * D;
   static constexpr int kVBytes = D * 64;
@@ -70,11 +90,11 @@ struct WsCfg {
   static constexpr int kSmemBytes = kOffTmem + 16 + 1024;  // + alignment slack
   static constexpr int kThreads = 256;
   // register split (setmaxnreg): the launch gives 128 per thread
-  static constexpr uint32_t kRegSoftmax = (D == 128) ? 88 : 128;
-  static constexpr uint32_t kRegPromote = (D == 128) ? 168 : 128;
+  static constexpr uint32_t kRegSoftmax = (D == 128) ? SA2PP_WS_REG_SOFTMAX : 128;
+  static constexpr uint32_t kRegPromote = (D == 128) ? 256 - SA2PP_WS_REG_SOFTMAX : 128;
+  static constexpr int kPvChunk16 = SA2PP_WS_PV_CHUNK;  // FP16-accumulator channels per TMEM load
   static_assert(kRegSoftmax + kRegPromote == 256, "the two warpgroups share the launch budget");
   static_assert(2 * kSmemBytes <= 227 * 1024, "two CTAs per SM must fit in shared memory");
-  static_assert((kStages & (kStages - 1)) == 0, "stage count must be a power of two");
 };
 
 template <int N, typename OutT>
@@ -167,6 +187,22 @@ __global__ void __launch_bounds__(256, 2)
   const uint32_t tm_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
   const int row_g = q0 + r;
   const bool row_valid = row_g < p.N;
+  // development trace (INSTR only): clock64 per (block < 64, warp, phase) of the first 8 tiles of head 0
+  unsigned long long* trc = (INSTR && p.trace != nullptr && bh == 0 && qt < 8 && lane == 0)
+                                ? p.trace + static_cast<int64_t>(qt) * 66 * 128 + warp * 16
+                                : nullptr;
+  auto stamp = [&](int j, int k) {
+    if constexpr (INSTR) {
+      if (trc != nullptr && j < 64) trc[(2 + j) * 128 + k] = clock64();
+    }
+  };
+  if constexpr (INSTR) {
+    if (trc != nullptr && threadIdx.x == 0) {
+      trc[0] = smid();
+      trc[1] = globaltimer();
+      trc[3] = nblk;
+    }
+  }
 
   if (warp < 4) {
     // =============================== softmax warpgroup ===============================
@@ -180,9 +216,11 @@ __global__ void __launch_bounds__(256, 2)
       constexpr bool MASK = decltype(mask_tag)::value;
       const int P = j & 1;
       const int st = static_cast<int>(static_cast<unsigned>(j) % S);
+      stamp(j, 0);
       mbar_wait_sleep(&kv_full[st], (static_cast<unsigned>(j) / S) & 1);  // bias / dK of this stage
       mbar_wait_sleep(&s_full[P], (j >> 1) & 1);
       tc_fence_after();
+      stamp(j, 1);
       const float* meta = reinterpret_cast<const float*>(smem + C::kOffMeta + st * C::kMetaBytes);
       const float* cb = reinterpret_cast<const float*>(smem + C::kOffBias + st * C::kBiasBytes);
       const uint32_t s_addr = tm_row + P * 64;
@@ -249,7 +287,9 @@ __global__ void __launch_bounds__(256, 2)
       // ---- tile scale (quantization.py:163-175): dP = max P~ / p_r = 2^Dt / p_r with
       //      Dt = max over the tile of (rowmax - m_new) <= 0, so P^ = P~ / dP = exp2(t - m_new + log2 p_r - Dt)
       //      in one exponential; l accumulates the unquantized P~ = P^ * dP (attention.py:149-153)
+      stamp(j, 2);
       mbar_wait(&dt_bar[P], (j >> 1) & 1);
+      stamp(j, 3);
       const float4 rv = ld_shared_f4(red + P * 4);
       float sh = fminf(fminf(rv.x, rv.y), fminf(rv.z, rv.w));  // -Dt >= 0
       sh = (sh == INFINITY) ? 0.0f : sh;
@@ -289,6 +329,7 @@ __global__ void __launch_bounds__(256, 2)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_ready[P]);  // release: alpha/dP stores and P^ in TMEM
+      stamp(j, 4);
       m_run = m_new;
     };
 
@@ -361,17 +402,58 @@ __global__ void __launch_bounds__(256, 2)
 #pragma unroll
     for (int c = 0; c < D / 2; ++c) O[c] = make_float2(0.0f, 0.0f);
 
+    // Software-pipelined promotion of the FP16 accumulator (production, INSTR off): the TMEM load of
+    // chunk c+1 (16 channels, 8 registers) is in flight while chunk c is converted and accumulated.
+    auto promote_pipe = [&](float alpha, auto resc_tag) {
+      constexpr bool RESC = decltype(resc_tag)::value;
+      const float2 al2 = make_float2(alpha, alpha);
+      constexpr int CH = 16, NC = D / CH;
+      uint32_t va[8], vb[8];
+      tmem_ld8_pack16(tm_row + C::kColPV, va);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        uint32_t(&cur)[8] = (c & 1) ? vb : va;
+        uint32_t(&nxt)[8] = (c & 1) ? va : vb;
+        if (c + 1 < NC) tmem_ld8_pack16(tm_row + C::kColPV + (c + 1) * CH, nxt);
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          const float4 fv = *reinterpret_cast<const float4*>(fw + c * CH + 2 * i);
+          const float2 p0 = f16x2_to_f32x2(cur[i]), p1 = f16x2_to_f32x2(cur[i + 1]);
+          float2& o0 = O[c * CH / 2 + i];
+          float2& o1 = O[c * CH / 2 + i + 1];
+          if constexpr (RESC) {
+            o0 = __ffma2_rn(p0, make_float2(fv.x, fv.y), __fmul2_rn(o0, al2));
+            o1 = __ffma2_rn(p1, make_float2(fv.z, fv.w), __fmul2_rn(o1, al2));
+          } else {
+            o0 = __ffma2_rn(p0, make_float2(fv.x, fv.y), o0);
+            o1 = __ffma2_rn(p1, make_float2(fv.z, fv.w), o1);
+          }
+        }
+        reg_fence16(reinterpret_cast<float*>(&O[c * CH / 2]));
+        if (c + 1 < NC) tmem_wait_ld();
+      }
+    };
     // O[c] = O[c]*alpha + pv[c]*f[c] for the row's D channels (attention.py:303).
     auto promote_impl = [&](int j, float alpha, auto resc_tag) {
       constexpr bool RESC = decltype(resc_tag)::value;
       const float2 al2 = make_float2(alpha, alpha);
-      constexpr int CH = ACC16 ? 32 : 16;  // channels per TMEM load (16 registers either way)
+      constexpr int CH = ACC16 ? C::kPvChunk16 : 16;  // channels per TMEM load
 #pragma unroll
       for (int c0 = 0; c0 < D; c0 += CH) {
+        float4 fpre[SA2PP_WS_F_PREFETCH ? CH / 4 : 1];
+        if constexpr (SA2PP_WS_F_PREFETCH != 0) {  // f of this chunk in flight beside the TMEM load
+#pragma unroll
+          for (int i = 0; i < CH / 4; ++i) fpre[i] = *reinterpret_cast<const float4*>(fw + c0 + 4 * i);
+        }
         float2 pv[CH / 2];
         if constexpr (ACC16) {
           uint32_t v[CH / 2];
-          tmem_ld16_pack16(tm_row + C::kColPV + c0, v);  // F16 accumulators, 2 per register
+          if constexpr (CH == 32) {
+            tmem_ld16_pack16(tm_row + C::kColPV + c0, v);  // F16 accumulators, 2 per register
+          } else {
+            tmem_ld8_pack16(tm_row + C::kColPV + c0, v);
+          }
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < CH / 2; ++i) pv[i] = f16x2_to_f32x2(v[i]);
@@ -398,7 +480,7 @@ __global__ void __launch_bounds__(256, 2)
         }
 #pragma unroll
         for (int i = 0; i < CH / 2; i += 2) {
-          const float4 fv = ld_shared_f4(fw + c0 + 2 * i);
+          const float4 fv = SA2PP_WS_F_PREFETCH ? fpre[SA2PP_WS_F_PREFETCH ? i / 2 : 0] : ld_shared_f4(fw + c0 + 2 * i);
           if constexpr (RESC) {
             O[c0 / 2 + i] = __ffma2_rn(pv[i], make_float2(fv.x, fv.y), __fmul2_rn(O[c0 / 2 + i], al2));
             O[c0 / 2 + i + 1] = __ffma2_rn(pv[i + 1], make_float2(fv.z, fv.w), __fmul2_rn(O[c0 / 2 + i + 1], al2));
@@ -417,11 +499,12 @@ __global__ void __launch_bounds__(256, 2)
 
     for (int j = 0; j < nblk; ++j) {
       const int st = static_cast<int>(static_cast<unsigned>(j) % S);
+      stamp(j, 0);
       if (warp == 4) {  // ---- issue PV(j), S(j+2) and the refill of block j-1's stage
         mbar_wait_sleep(&p_ready[j & 1], (j >> 1) & 1);
         if (j > 0) mbar_wait(pv_free, (j - 1) & 1);
         tc_fence_after();
-        if (elect_one()) {
+        if (elect_one()) {  // one elected region: every UTC* op in a divergent region pays an ELECT loop
           issue_pv(j);
           if (j + 2 < nblk) {
             mbar_wait(&kv_full[static_cast<unsigned>(j + 2) % S], (static_cast<unsigned>(j + 2) / S) & 1);
@@ -433,8 +516,15 @@ __global__ void __launch_bounds__(256, 2)
       }
       // ---- promotion of block j: f[c] = dP_j * dV_j[c] for this warp's copy
       mbar_wait_sleep(&kv_full[st], (static_cast<unsigned>(j) / S) & 1);  // dV of this stage visible
-      mbar_wait_sleep(pv_full, static_cast<uint32_t>(j) & 1u);
+      stamp(j, 1);
+      if constexpr (SA2PP_WS_FANOUT != 0) {  // one warp polls the MMA barrier, the others sleep in bar.sync
+        if (warp == 4) mbar_wait(pv_full, static_cast<uint32_t>(j) & 1u);
+        named_bar_sync(1, 128);
+      } else {
+        mbar_wait_sleep(pv_full, static_cast<uint32_t>(j) & 1u);
+      }
       tc_fence_after();
+      stamp(j, 2);
       const float dP = dp_s[j & 3];
       const float alpha = alpha_s[(j & 3) * 128 + r];
       {
@@ -446,14 +536,24 @@ __global__ void __launch_bounds__(256, 2)
         }
       }
       __syncwarp();
+      constexpr bool kPipe = SA2PP_WS_PIPE != 0 && ACC16 && !INSTR;
       if (__any_sync(0xffffffffu, alpha != 1.0f)) {
-        promote_impl(j, alpha, std::true_type{});
+        if constexpr (kPipe) {
+          promote_pipe(alpha, std::true_type{});
+        } else {
+          promote_impl(j, alpha, std::true_type{});
+        }
       } else {
-        promote_impl(j, alpha, std::false_type{});
+        if constexpr (kPipe) {
+          promote_pipe(alpha, std::false_type{});
+        } else {
+          promote_impl(j, alpha, std::false_type{});
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(pv_free);
+      stamp(j, 3);
     }
     if (want_overflow && overflow) atomicAdd(&p.report->overflow_events, overflow);
     // ---- O / l (attention.py:304-305)
@@ -468,6 +568,9 @@ __global__ void __launch_bounds__(256, 2)
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (INSTR) {
+    if (trc != nullptr && threadIdx.x == 0) trc[2] = globaltimer();
+  }
   if (warp == 0) {
     tc_fence_after();
     tmem_dealloc(tmem, C::kTmemCols);
@@ -510,7 +613,8 @@ static cudaError_t launch_ws_outi(const AttnParams& P, const sa2pp_quant& qt, cu
 
 template <int D, bool CAUSAL, bool ACC16>
 static cudaError_t launch_ws_out(const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
-  if (P.debug != nullptr || P.report != nullptr) return launch_ws_outi<D, CAUSAL, ACC16, true>(P, qt, st);
+  if (P.debug != nullptr || P.report != nullptr || P.trace != nullptr)
+    return launch_ws_outi<D, CAUSAL, ACC16, true>(P, qt, st);
   return launch_ws_outi<D, CAUSAL, ACC16, false>(P, qt, st);
 }
 

@@ -248,7 +248,7 @@ int sa2pp_attn_fwd(const sa2pp_problem* p, const sa2pp_quant* qt, const sa2pp_ou
     const char* v = std::getenv("SA2PP_ATTN");
     return v != nullptr && std::strcmp(v, "v4") == 0;
   }();
-  cudaError_t e = use_v4 || P.trace != nullptr ? sa2pp::launch_attn(*p, P, *qt, static_cast<cudaStream_t>(stream))
+  cudaError_t e = use_v4 ? sa2pp::launch_attn(*p, P, *qt, static_cast<cudaStream_t>(stream))
                                                 : sa2pp::launch_attn_ws(*p, P, *qt, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return SA2PP_OK;
