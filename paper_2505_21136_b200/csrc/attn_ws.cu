@@ -53,6 +53,9 @@
 #ifndef SA2PP_WS_PIPE
 #define SA2PP_WS_PIPE 1
 #endif
+#ifndef SA2PP_WS_SPLIT_ISSUE
+#define SA2PP_WS_SPLIT_ISSUE 0
+#endif
 #ifndef SA2PP_WS_STAGES128
 #define SA2PP_WS_STAGES128 4
 #endif
@@ -73,6 +76,9 @@ struct WsCfg {
   static constexpr uint32_t kSboV = 512;
   static constexpr int kTmemCols = 256;
   static constexpr int kColPV = 128;
+  // D=64 leaves room for two PV accumulators (128 + 2*64 = 256 columns): PV(j+1) then runs while
+  // block j is promoted.  D=128 has one.
+  static constexpr int kNumPV = (D == 64) ? 2 : 1;
   // shared memory carve-up (offsets from a 1024-aligned base)
   static constexpr int kOffQ = 0;
   static constexpr int kOffK = kOffQ + kQBytes;
@@ -85,7 +91,7 @@ struct WsCfg {
   static constexpr int kOffRed = kOffDp + 4 * 4;                  // [2][4] per-warp max-shift candidates
   static constexpr int kOffL = kOffRed + 2 * 4 * 4;               // [128] final row sums
   static constexpr int kOffBar = kOffL + 128 * 4;
-  static constexpr int kNumBars = 1 + kStages + 2 + 2 + 1 + 1 + 2 + 1;
+  static constexpr int kNumBars = 1 + kStages + 2 + 2 + 2 * kNumPV + 2 + 1;
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmemBytes = kOffTmem + 16 + 1024;  // + alignment slack
   static constexpr int kThreads = 256;
@@ -151,9 +157,9 @@ __global__ void __launch_bounds__(256, 2)
   uint64_t* kv_full = q_full + 1;    // [S] TMA landed
   uint64_t* s_full = kv_full + S;    // [2] S(j) in TMEM
   uint64_t* p_ready = s_full + 2;    // [2] the 4 softmax warps stored P^(j) and published alpha_j, dP_j
-  uint64_t* pv_full = p_ready + 2;   // [1] PV(j) in TMEM
-  uint64_t* pv_free = pv_full + 1;   // [1] the 4 promotion warps drained PV(j)
-  uint64_t* dt_bar = pv_free + 1;    // [2] the 4 softmax warps published their max-shift
+  uint64_t* pv_full = p_ready + 2;          // [kNumPV] PV(j) in TMEM buffer j % kNumPV
+  uint64_t* pv_free = pv_full + C::kNumPV;  // [kNumPV] the 4 promotion warps drained that buffer
+  uint64_t* dt_bar = pv_free + C::kNumPV;   // [2] the 4 softmax warps published their max-shift
   uint64_t* l_ready = dt_bar + 2;    // [1] final row sums written
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + C::kOffTmem);
   float* alpha_s = reinterpret_cast<float*>(smem + C::kOffAlpha);
@@ -170,8 +176,10 @@ __global__ void __launch_bounds__(256, 2)
         mbar_init(&p_ready[x], 4);
         mbar_init(&dt_bar[x], 4);
       }
-      mbar_init(pv_full, 1);
-      mbar_init(pv_free, 4);
+      for (int x = 0; x < C::kNumPV; ++x) {
+        mbar_init(&pv_full[x], 1);
+        mbar_init(&pv_free[x], 4);
+      }
       mbar_init(l_ready, 4);
       fence_barrier_init();
     }
@@ -372,9 +380,10 @@ __global__ void __launch_bounds__(256, 2)
       const int st = static_cast<int>(static_cast<unsigned>(j) % S);
       const uint64_t vdesc = smem_desc(smem_u32(smem + C::kOffV + st * C::kVBytes), C::kSboV, C::kLayoutV);
       const uint32_t a_tm = tmem + (j & 1) * 64;
-      umma_f8_ts(tmem + C::kColPV, a_tm, vdesc, idesc_pv, 0u);           // keys  0..31: P^ cols [0,8)
-      umma_f8_ts(tmem + C::kColPV, a_tm + 8, vdesc + 2, idesc_pv, 1u);   // keys 32..63: P^ cols [8,16)
-      umma_commit(pv_full);
+      const int pb = j % C::kNumPV;
+      umma_f8_ts(tmem + C::kColPV + pb * D, a_tm, vdesc, idesc_pv, 0u);          // keys  0..31: P^ cols [0,8)
+      umma_f8_ts(tmem + C::kColPV + pb * D, a_tm + 8, vdesc + 2, idesc_pv, 1u);  // keys 32..63: P^ cols [8,16)
+      umma_commit(&pv_full[pb]);
     };
     if (warp == 4 && elect_one()) {
       tma_prefetch_desc(&tm_q);
@@ -404,18 +413,18 @@ __global__ void __launch_bounds__(256, 2)
 
     // Software-pipelined promotion of the FP16 accumulator (production, INSTR off): the TMEM load of
     // chunk c+1 (16 channels, 8 registers) is in flight while chunk c is converted and accumulated.
-    auto promote_pipe = [&](float alpha, auto resc_tag) {
+    auto promote_pipe = [&](uint32_t pv_col, float alpha, auto resc_tag) {
       constexpr bool RESC = decltype(resc_tag)::value;
       const float2 al2 = make_float2(alpha, alpha);
       constexpr int CH = 16, NC = D / CH;
       uint32_t va[8], vb[8];
-      tmem_ld8_pack16(tm_row + C::kColPV, va);
+      tmem_ld8_pack16(tm_row + pv_col, va);
       tmem_wait_ld();
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
         uint32_t(&cur)[8] = (c & 1) ? vb : va;
         uint32_t(&nxt)[8] = (c & 1) ? va : vb;
-        if (c + 1 < NC) tmem_ld8_pack16(tm_row + C::kColPV + (c + 1) * CH, nxt);
+        if (c + 1 < NC) tmem_ld8_pack16(tm_row + pv_col + (c + 1) * CH, nxt);
 #pragma unroll
         for (int i = 0; i < 8; i += 2) {
           const float4 fv = *reinterpret_cast<const float4*>(fw + c * CH + 2 * i);
@@ -435,7 +444,7 @@ __global__ void __launch_bounds__(256, 2)
       }
     };
     // O[c] = O[c]*alpha + pv[c]*f[c] for the row's D channels (attention.py:303).
-    auto promote_impl = [&](int j, float alpha, auto resc_tag) {
+    auto promote_impl = [&](int j, uint32_t pv_col, float alpha, auto resc_tag) {
       constexpr bool RESC = decltype(resc_tag)::value;
       const float2 al2 = make_float2(alpha, alpha);
       constexpr int CH = ACC16 ? C::kPvChunk16 : 16;  // channels per TMEM load
@@ -450,9 +459,9 @@ __global__ void __launch_bounds__(256, 2)
         if constexpr (ACC16) {
           uint32_t v[CH / 2];
           if constexpr (CH == 32) {
-            tmem_ld16_pack16(tm_row + C::kColPV + c0, v);  // F16 accumulators, 2 per register
+            tmem_ld16_pack16(tm_row + pv_col + c0, v);  // F16 accumulators, 2 per register
           } else {
-            tmem_ld8_pack16(tm_row + C::kColPV + c0, v);
+            tmem_ld8_pack16(tm_row + pv_col + c0, v);
           }
           tmem_wait_ld();
 #pragma unroll
@@ -464,7 +473,7 @@ __global__ void __launch_bounds__(256, 2)
           }
         } else {
           uint32_t v[CH];
-          tmem_ld16(tm_row + C::kColPV + c0, v);
+          tmem_ld16(tm_row + pv_col + c0, v);
           tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < CH / 2; ++i) pv[i] = make_float2(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
@@ -502,15 +511,18 @@ __global__ void __launch_bounds__(256, 2)
       stamp(j, 0);
       if (warp == 4) {  // ---- issue PV(j), S(j+2) and the refill of block j-1's stage
         mbar_wait_sleep(&p_ready[j & 1], (j >> 1) & 1);
-        if (j > 0) mbar_wait(pv_free, (j - 1) & 1);
+        if (j >= C::kNumPV) mbar_wait(&pv_free[j % C::kNumPV], (j / C::kNumPV - 1) & 1);
         tc_fence_after();
         if (elect_one()) {  // one elected region: every UTC* op in a divergent region pays an ELECT loop
           issue_pv(j);
-          if (j + 2 < nblk) {
-            mbar_wait(&kv_full[static_cast<unsigned>(j + 2) % S], (static_cast<unsigned>(j + 2) / S) & 1);
-            issue_qk(j + 2);
+          if (!SA2PP_WS_SPLIT_ISSUE) {
+            if (j + 2 < nblk) {
+              mbar_wait(&kv_full[static_cast<unsigned>(j + 2) % S], (static_cast<unsigned>(j + 2) / S) & 1);
+              issue_qk(j + 2);
+            }
+            // the stage of block j-kNumPV: its promotion was waited for just above
+          if (j >= C::kNumPV && j - C::kNumPV + S < nblk) load_block(j - C::kNumPV + S);
           }
-          if (j >= 1 && j - 1 + S < nblk) load_block(j - 1 + S);
         }
         __syncwarp();
       }
@@ -518,13 +530,28 @@ __global__ void __launch_bounds__(256, 2)
       mbar_wait_sleep(&kv_full[st], (static_cast<unsigned>(j) / S) & 1);  // dV of this stage visible
       stamp(j, 1);
       if constexpr (SA2PP_WS_FANOUT != 0) {  // one warp polls the MMA barrier, the others sleep in bar.sync
-        if (warp == 4) mbar_wait(pv_full, static_cast<uint32_t>(j) & 1u);
+        if (warp == 4) mbar_wait(&pv_full[j % C::kNumPV], static_cast<uint32_t>(j / C::kNumPV) & 1u);
         named_bar_sync(1, 128);
       } else {
-        mbar_wait_sleep(pv_full, static_cast<uint32_t>(j) & 1u);
+        mbar_wait_sleep(&pv_full[j % C::kNumPV], static_cast<uint32_t>(j / C::kNumPV) & 1u);
       }
       tc_fence_after();
       stamp(j, 2);
+      if constexpr (SA2PP_WS_SPLIT_ISSUE != 0) {
+        // PV(j) has completed, so S[j&1] (P^(j)) and block j-1's stage are free: warp 5 issues S(j+2),
+        // warp 6 the refill, so the issue cost is spread over the promotion warps
+        if (warp == 5 && j + 2 < nblk) {
+          if (elect_one()) {
+            mbar_wait(&kv_full[static_cast<unsigned>(j + 2) % S], (static_cast<unsigned>(j + 2) / S) & 1);
+            issue_qk(j + 2);
+          }
+          __syncwarp();
+        }
+        if (warp == 6 && j >= 1 && j - 1 + S < nblk) {
+          if (elect_one()) load_block(j - 1 + S);
+          __syncwarp();
+        }
+      }
       const float dP = dp_s[j & 3];
       const float alpha = alpha_s[(j & 3) * 128 + r];
       {
@@ -539,20 +566,20 @@ __global__ void __launch_bounds__(256, 2)
       constexpr bool kPipe = SA2PP_WS_PIPE != 0 && ACC16 && !INSTR;
       if (__any_sync(0xffffffffu, alpha != 1.0f)) {
         if constexpr (kPipe) {
-          promote_pipe(alpha, std::true_type{});
+          promote_pipe(C::kColPV + (j % C::kNumPV) * D, alpha, std::true_type{});
         } else {
-          promote_impl(j, alpha, std::true_type{});
+          promote_impl(j, C::kColPV + (j % C::kNumPV) * D, alpha, std::true_type{});
         }
       } else {
         if constexpr (kPipe) {
-          promote_pipe(alpha, std::false_type{});
+          promote_pipe(C::kColPV + (j % C::kNumPV) * D, alpha, std::false_type{});
         } else {
-          promote_impl(j, alpha, std::false_type{});
+          promote_impl(j, C::kColPV + (j % C::kNumPV) * D, alpha, std::false_type{});
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(pv_free);
+      if (lane == 0) mbar_arrive(&pv_free[j % C::kNumPV]);
       stamp(j, 3);
     }
     if (want_overflow && overflow) atomicAdd(&p.report->overflow_events, overflow);
