@@ -47,14 +47,8 @@
 #ifndef SA2PP_WS_F_PREFETCH
 #define SA2PP_WS_F_PREFETCH 0
 #endif
-#ifndef SA2PP_WS_FANOUT
-#define SA2PP_WS_FANOUT 0
-#endif
 #ifndef SA2PP_WS_PIPE
 #define SA2PP_WS_PIPE 1
-#endif
-#ifndef SA2PP_WS_SPLIT_ISSUE
-#define SA2PP_WS_SPLIT_ISSUE 0
 #endif
 #ifndef SA2PP_WS_STAGES128
 #define SA2PP_WS_STAGES128 4
@@ -131,7 +125,7 @@ __device__ __forceinline__ void store_row(OutT* dst, const float2 (&O)[N / 2], f
   }
 }
 
-template <int D, bool CAUSAL, bool ACC16, bool INSTR, typename OutT>
+template <int D, bool CAUSAL, bool ACC16, bool INSTR, typename OutT, int G>
 __global__ void __launch_bounds__(256, 2)
     attn_ws_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                    const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
@@ -376,13 +370,18 @@ __global__ void __launch_bounds__(256, 2)
       for (int kk = 0; kk < D / 32; ++kk) umma_i8_ss(d_tm, qdesc + 2 * kk, kdesc + 2 * kk, idesc_qk, kk > 0 ? 1u : 0u);
       umma_commit(&s_full[j & 1]);
     };
-    auto issue_pv = [&](int j) {  // one thread; P^(j) stored, PV(j-1) drained
+    auto issue_pv = [&](int u, int j, int g) {  // one thread; P^(j) stored, the PV buffer drained
       const int st = static_cast<int>(static_cast<unsigned>(j) % S);
       const uint64_t vdesc = smem_desc(smem_u32(smem + C::kOffV + st * C::kVBytes), C::kSboV, C::kLayoutV);
       const uint32_t a_tm = tmem + (j & 1) * 64;
-      const int pb = j % C::kNumPV;
-      umma_f8_ts(tmem + C::kColPV + pb * D, a_tm, vdesc, idesc_pv, 0u);          // keys  0..31: P^ cols [0,8)
-      umma_f8_ts(tmem + C::kColPV + pb * D, a_tm + 8, vdesc + 2, idesc_pv, 1u);  // keys 32..63: P^ cols [8,16)
+      const int pb = u % C::kNumPV;
+      const uint32_t d_tm = tmem + C::kColPV + pb * D;
+      if (G == 1) {  // depth 2: the two k=32 groups chain in the FP16 (or FP32) accumulator
+        umma_f8_ts(d_tm, a_tm, vdesc, idesc_pv, 0u);          // keys  0..31: P^ cols [0,8)
+        umma_f8_ts(d_tm, a_tm + 8, vdesc + 2, idesc_pv, 1u);  // keys 32..63: P^ cols [8,16)
+      } else {       // depth 1: group g alone
+        umma_f8_ts(d_tm, a_tm + 8 * g, vdesc + 2 * g, idesc_pv, 0u);
+      }
       umma_commit(&pv_full[pb]);
     };
     if (warp == 4 && elect_one()) {
@@ -506,55 +505,43 @@ __global__ void __launch_bounds__(256, 2)
       }
     };
 
-    for (int j = 0; j < nblk; ++j) {
+    // Sub-blocks: G = 1 normally; G = 2 for buffering depth 1 with the FP16 accumulator
+    // (mma.py:144-152): each k=32 group of a block is its own FP16 accumulation, converted to FP32
+    // and promoted on its own (the FP32 sum of the two groups is formed in O instead of in a
+    // temporary, which differs only by FP32 rounding).
+    for (int u = 0; u < nblk * G; ++u) {
+      const int j = (G == 1) ? u : (u >> 1);
+      const int g = (G == 1) ? 0 : (u & 1);
       const int st = static_cast<int>(static_cast<unsigned>(j) % S);
+      const int pb = u % C::kNumPV;
       stamp(j, 0);
-      if (warp == 4) {  // ---- issue PV(j), S(j+2) and the refill of block j-1's stage
-        mbar_wait_sleep(&p_ready[j & 1], (j >> 1) & 1);
-        if (j >= C::kNumPV) mbar_wait(&pv_free[j % C::kNumPV], (j / C::kNumPV - 1) & 1);
+      if (warp == 4) {  // ---- issue PV(j) [group g], S(j+2) and the refill of block j-1's stage
+        if (g == 0) mbar_wait_sleep(&p_ready[j & 1], (j >> 1) & 1);
+        if (u >= C::kNumPV) mbar_wait(&pv_free[pb], (u / C::kNumPV - 1) & 1);
         tc_fence_after();
         if (elect_one()) {  // one elected region: every UTC* op in a divergent region pays an ELECT loop
-          issue_pv(j);
-          if (!SA2PP_WS_SPLIT_ISSUE) {
+          issue_pv(u, j, g);
+          if (g == G - 1) {  // P^(j) fully consumed once the last group's MMA is issued (in order)
             if (j + 2 < nblk) {
               mbar_wait(&kv_full[static_cast<unsigned>(j + 2) % S], (static_cast<unsigned>(j + 2) / S) & 1);
               issue_qk(j + 2);
             }
-            // the stage of block j-kNumPV: its promotion was waited for just above
-          if (j >= C::kNumPV && j - C::kNumPV + S < nblk) load_block(j - C::kNumPV + S);
           }
+          // the stage of block j-1: the promotion that last read it was waited for just above
+          const int jr = (u - C::kNumPV) / G;  // block whose promotion is complete
+          if (u >= C::kNumPV && (u - C::kNumPV) % G == G - 1 && jr + S < nblk) load_block(jr + S);
         }
         __syncwarp();
       }
-      // ---- promotion of block j: f[c] = dP_j * dV_j[c] for this warp's copy
+      // ---- promotion of block j (group g): f[c] = dP_j * dV_j[c] for this warp's copy
       mbar_wait_sleep(&kv_full[st], (static_cast<unsigned>(j) / S) & 1);  // dV of this stage visible
       stamp(j, 1);
-      if constexpr (SA2PP_WS_FANOUT != 0) {  // one warp polls the MMA barrier, the others sleep in bar.sync
-        if (warp == 4) mbar_wait(&pv_full[j % C::kNumPV], static_cast<uint32_t>(j / C::kNumPV) & 1u);
-        named_bar_sync(1, 128);
-      } else {
-        mbar_wait_sleep(&pv_full[j % C::kNumPV], static_cast<uint32_t>(j / C::kNumPV) & 1u);
-      }
+      mbar_wait_sleep(&pv_full[pb], static_cast<uint32_t>(u / C::kNumPV) & 1u);
       tc_fence_after();
       stamp(j, 2);
-      if constexpr (SA2PP_WS_SPLIT_ISSUE != 0) {
-        // PV(j) has completed, so S[j&1] (P^(j)) and block j-1's stage are free: warp 5 issues S(j+2),
-        // warp 6 the refill, so the issue cost is spread over the promotion warps
-        if (warp == 5 && j + 2 < nblk) {
-          if (elect_one()) {
-            mbar_wait(&kv_full[static_cast<unsigned>(j + 2) % S], (static_cast<unsigned>(j + 2) / S) & 1);
-            issue_qk(j + 2);
-          }
-          __syncwarp();
-        }
-        if (warp == 6 && j >= 1 && j - 1 + S < nblk) {
-          if (elect_one()) load_block(j - 1 + S);
-          __syncwarp();
-        }
-      }
       const float dP = dp_s[j & 3];
-      const float alpha = alpha_s[(j & 3) * 128 + r];
-      {
+      const float alpha = g == 0 ? alpha_s[(j & 3) * 128 + r] : 1.0f;
+      if (g == 0) {
         const float* meta = reinterpret_cast<const float*>(smem + C::kOffMeta + st * C::kMetaBytes);
 #pragma unroll
         for (int c = 4 * lane; c < D; c += 128) {
@@ -564,22 +551,23 @@ __global__ void __launch_bounds__(256, 2)
       }
       __syncwarp();
       constexpr bool kPipe = SA2PP_WS_PIPE != 0 && ACC16 && !INSTR;
+      const uint32_t pv_col = C::kColPV + pb * D;
       if (__any_sync(0xffffffffu, alpha != 1.0f)) {
         if constexpr (kPipe) {
-          promote_pipe(C::kColPV + (j % C::kNumPV) * D, alpha, std::true_type{});
+          promote_pipe(pv_col, alpha, std::true_type{});
         } else {
-          promote_impl(j, C::kColPV + (j % C::kNumPV) * D, alpha, std::true_type{});
+          promote_impl(j, pv_col, alpha, std::true_type{});
         }
       } else {
         if constexpr (kPipe) {
-          promote_pipe(C::kColPV + (j % C::kNumPV) * D, alpha, std::false_type{});
+          promote_pipe(pv_col, alpha, std::false_type{});
         } else {
-          promote_impl(j, C::kColPV + (j % C::kNumPV) * D, alpha, std::false_type{});
+          promote_impl(j, pv_col, alpha, std::false_type{});
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&pv_free[j % C::kNumPV]);
+      if (lane == 0) mbar_arrive(&pv_free[pb]);
       stamp(j, 3);
     }
     if (want_overflow && overflow) atomicAdd(&p.report->overflow_events, overflow);
@@ -605,7 +593,7 @@ __global__ void __launch_bounds__(256, 2)
 }
 
 // ------------------------------------------------------------------ host side
-template <int D, bool CAUSAL, bool ACC16, bool INSTR, typename OutT>
+template <int D, bool CAUSAL, bool ACC16, bool INSTR, typename OutT, int G>
 static cudaError_t launch_ws_t(const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
   using C = WsCfg<D>;
   CUtensorMap mq, mk, mv;
@@ -615,7 +603,7 @@ static cudaError_t launch_ws_t(const AttnParams& P, const sa2pp_quant& qt, cudaS
       !make_map_2d(&mv, qt.v_codes, P.Np, static_cast<uint64_t>(P.B) * P.Hkv * D, P.Np, 64, D,
                    CU_TENSOR_MAP_SWIZZLE_64B))
     return cudaErrorInvalidValue;
-  auto kern = attn_ws_kernel<D, CAUSAL, ACC16, INSTR, OutT>;
+  auto kern = attn_ws_kernel<D, CAUSAL, ACC16, INSTR, OutT, G>;
   static PerDevice once;
   cudaError_t e = once.run([&](std::atomic<int>&) {
     cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
@@ -628,31 +616,34 @@ static cudaError_t launch_ws_t(const AttnParams& P, const sa2pp_quant& qt, cudaS
   return cudaGetLastError();
 }
 
-template <int D, bool CAUSAL, bool ACC16, bool INSTR>
+template <int D, bool CAUSAL, bool ACC16, bool INSTR, int G>
 static cudaError_t launch_ws_outi(const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
   switch (P.out_dtype) {
-    case SA2PP_F32: return launch_ws_t<D, CAUSAL, ACC16, INSTR, float>(P, qt, st);
-    case SA2PP_F16: return launch_ws_t<D, CAUSAL, ACC16, INSTR, __half>(P, qt, st);
-    case SA2PP_BF16: return launch_ws_t<D, CAUSAL, ACC16, INSTR, __nv_bfloat16>(P, qt, st);
+    case SA2PP_F32: return launch_ws_t<D, CAUSAL, ACC16, INSTR, float, G>(P, qt, st);
+    case SA2PP_F16: return launch_ws_t<D, CAUSAL, ACC16, INSTR, __half, G>(P, qt, st);
+    case SA2PP_BF16: return launch_ws_t<D, CAUSAL, ACC16, INSTR, __nv_bfloat16, G>(P, qt, st);
     default: return cudaErrorInvalidValue;
   }
 }
 
-template <int D, bool CAUSAL, bool ACC16>
+template <int D, bool CAUSAL, bool ACC16, int G>
 static cudaError_t launch_ws_out(const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
   if (P.debug != nullptr || P.report != nullptr || P.trace != nullptr)
-    return launch_ws_outi<D, CAUSAL, ACC16, true>(P, qt, st);
-  return launch_ws_outi<D, CAUSAL, ACC16, false>(P, qt, st);
+    return launch_ws_outi<D, CAUSAL, ACC16, true, G>(P, qt, st);
+  return launch_ws_outi<D, CAUSAL, ACC16, false, G>(P, qt, st);
 }
 
 template <int D>
 static cudaError_t launch_ws_d(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt,
                                cudaStream_t st) {
   const bool acc16 = prob.pv_accum == SA2PP_ACC_F16;
-  if (prob.causal) {
-    return acc16 ? launch_ws_out<D, true, true>(P, qt, st) : launch_ws_out<D, true, false>(P, qt, st);
+  if (acc16 && prob.buffering_depth == 1) {  // FP16 accumulation per k=32 group (mma.py:144-152)
+    return prob.causal ? launch_ws_out<D, true, true, 2>(P, qt, st) : launch_ws_out<D, false, true, 2>(P, qt, st);
   }
-  return acc16 ? launch_ws_out<D, false, true>(P, qt, st) : launch_ws_out<D, false, false>(P, qt, st);
+  if (prob.causal) {
+    return acc16 ? launch_ws_out<D, true, true, 1>(P, qt, st) : launch_ws_out<D, true, false, 1>(P, qt, st);
+  }
+  return acc16 ? launch_ws_out<D, false, true, 1>(P, qt, st) : launch_ws_out<D, false, false, 1>(P, qt, st);
 }
 
 cudaError_t launch_attn_ws(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {

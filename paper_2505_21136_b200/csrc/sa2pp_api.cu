@@ -106,10 +106,6 @@ int sa2pp_check_problem(const sa2pp_problem* p) {
   if (!p->expect_overflow && p->p_r * p->v_r > bound)
     return fail(SA2PP_ERR_RANGE, "p_r*v_r = %g > %g (FP16 accumulator bound at buffering depth %d)",
                 p->p_r * p->v_r, bound, p->buffering_depth);
-  if (p->pv_accum == SA2PP_ACC_F16 && p->buffering_depth == 1)
-    return fail(SA2PP_ERR_UNSUPPORTED,
-                "buffering_depth 1 with the FP16 accumulator is not built: tcgen05 accumulates the "
-                "64-key block in one FP16 register (depth 2)");
   if (p->batch * static_cast<int64_t>(p->heads_q) > 65535)
     return fail(SA2PP_ERR_UNSUPPORTED, "batch*heads_q must be <= 65535");
   return SA2PP_OK;
@@ -244,11 +240,13 @@ int sa2pp_attn_fwd(const sa2pp_problem* p, const sa2pp_quant* qt, const sa2pp_ou
   P.report = report;
   P.debug = g_debug;
   P.trace = g_trace;
+  // the v4 kernel chains both k=32 groups in one FP16 accumulator (depth 2 only)
+  const bool depth1_f16 = p->pv_accum == SA2PP_ACC_F16 && p->buffering_depth == 1;
   static const bool use_v4 = [] {
     const char* v = std::getenv("SA2PP_ATTN");
     return v != nullptr && std::strcmp(v, "v4") == 0;
   }();
-  cudaError_t e = use_v4 ? sa2pp::launch_attn(*p, P, *qt, static_cast<cudaStream_t>(stream))
+  cudaError_t e = use_v4 && !depth1_f16 ? sa2pp::launch_attn(*p, P, *qt, static_cast<cudaStream_t>(stream))
                                                 : sa2pp::launch_attn_ws(*p, P, *qt, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   return SA2PP_OK;

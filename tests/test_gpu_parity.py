@@ -22,9 +22,7 @@ if not gpu_ready():
 import paper_2505_21136_b200 as sa  # noqa: E402
 from oracle import sage_cpu as oc  # noqa: E402
 
-SUPPORTED = [n for n in golden_cases()
-             if golden_config(load_golden(n))["dim"] in (64, 128)
-             and not (golden_config(load_golden(n))["pv"] == "fp16" and golden_config(load_golden(n))["depth"] == 1)]
+SUPPORTED = [n for n in golden_cases() if golden_config(load_golden(n))["dim"] in (64, 128)]
 
 
 def run_case(g, dtype=torch.float32, layout="HND"):

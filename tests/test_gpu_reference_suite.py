@@ -3,9 +3,8 @@ run through the B200 `attention_quantized` mirror with the same assertions.
 
 The reference uses head_dim 32 there; the sm_100a kernels are built for head_dim 64 and 128
 (SA2PP_ERR_UNSUPPORTED otherwise), so the cases run at 64 with the reference's seeds,
-shapes and thresholds otherwise unchanged.  The reference's depth-1 FP16 conversion-halving case has
-no GPU counterpart (tcgen05 accumulates a 64-key block in one FP16 register, depth 2) and is checked
-on the analytic counters in tests/test_abi_cpu.py instead.
+shapes and thresholds otherwise unchanged.  Buffering depth 1 with the FP16 accumulator runs each
+k=32 group as its own tcgen05 MMA into a fresh FP16 accumulator, converted and promoted on its own.
 """
 
 import numpy as np
@@ -80,6 +79,21 @@ def test_int4_mode():  # test_attention.py:210-215
     rep = sa.attention_quantized(q, k, v, cfg)
     cos, _, _ = sa.compare(exact(q, k, v, cfg), rep.output)
     assert cos >= 0.95
+
+
+def test_conversion_halving_at_run_level():  # test_attention.py:217-230
+    q, k, v = gaussian_qkv(44, 1, 128, D)
+    reports = {}
+    for depth in (1, 2):
+        config = sa.AttentionConfig(seq_len=128, head_dim=D, range=sa.RangeConfig(224.0, 4.5, depth))
+        reports[depth] = sa.attention_quantized(q, k, v, config)
+    assert reports[1].fp16_to_fp32_conversions == 2 * reports[2].fp16_to_fp32_conversions
+    assert reports[1].mma_invocations == reports[2].mma_invocations
+    # the depth-1 run is a real FP16-per-group computation on the GPU: close to depth 2 and to the oracle
+    cfg = oc.AttentionConfig(seq_len=128, head_dim=D, range=oc.RangeConfig(224.0, 4.5, 1))
+    want = oc.attention_quantized(q, k, v, cfg).output
+    assert sa.compare(want, reports[1].output)[0] >= 0.9999
+    assert sa.compare(reports[2].output, reports[1].output)[0] >= 0.9999
 
 
 def test_fp32_baseline_close_to_fp16_path():  # test_attention.py:232-245
