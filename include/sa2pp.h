@@ -122,15 +122,35 @@ typedef struct {
 } sa2pp_output;
 
 /* Optional run report, device-resident (attention.py:114-125 RunReport analogue).
- * Pass NULL to skip.  Zero it before the call; the kernel accumulates into it. */
+ * Pass NULL to skip.  Initialise it with sa2pp_report_init (or: overflow 0, p_scale_min_bits
+ * 0x7f800000, p_scale_max_bits 0, v_scale_min_bits 0x7ff0000000000000, v_scale_max_bits 0) before the
+ * first call; the kernels accumulate into it, so one report can span several calls. */
 typedef struct {
   uint32_t overflow_events;   /* non-finite FP16 partials seen at promotion */
-  uint32_t p_scale_min_bits;  /* float bits of min / max delta_P over all tiles (init 0x7f800000 / 0) */
+  uint32_t p_scale_min_bits;  /* float bits of min / max delta_P over all (query tile, key block) */
   uint32_t p_scale_max_bits;
   uint32_t reserved;
+  uint64_t v_scale_min_bits;  /* double bits of min / max delta_V over all (key block, channel) */
+  uint64_t v_scale_max_bits;
 } sa2pp_report;
 
+/* Host-side run report of a host-pipeline call: the reference's RunReport fields
+ * (attention.py:114-125).  Conversions and MMA invocations are the reference's analytic counts
+ * (mma.py:67-86); the rest are measured on the device. */
+typedef struct {
+  uint64_t overflow_events;
+  uint64_t fp16_to_fp32_conversions;
+  uint64_t mma_invocations;
+  double p_scale_min, p_scale_max;
+  double v_scale_min, v_scale_max;
+} sa2pp_run_report;
+
 SA2PP_API int sa2pp_version(void);
+/* Reference-exact counters of one call (attention_quantized's fp16_to_fp32_conversions and
+ * mma_invocations, mma.py:67-86), host-only arithmetic. */
+SA2PP_API int sa2pp_analytic_counts(const sa2pp_problem* prob, uint64_t* conversions, uint64_t* mma_invocations);
+/* Write the initial values of a device sa2pp_report (stream-ordered). */
+SA2PP_API int sa2pp_report_init(sa2pp_report* report, void* cuda_stream);
 SA2PP_API const char* sa2pp_last_error(void);
 
 /* Validate the problem (shapes, head_dim, range rule).  No device work. */
@@ -167,6 +187,10 @@ SA2PP_API int sa2pp_host_pipeline_create(const sa2pp_problem* prob, int dtype, i
                                          sa2pp_host_pipeline** out);
 SA2PP_API int sa2pp_host_pipeline_run(sa2pp_host_pipeline* hp, const void* q, const void* k, const void* v, void* o,
                                       void* cuda_stream);
+/* The same computation with the instrumented kernels, blocking until O is in host memory, filling
+ * `report` (attention_quantized's RunReport).  Slower than run(): for parity and accounting. */
+SA2PP_API int sa2pp_host_pipeline_run_report(sa2pp_host_pipeline* hp, const void* q, const void* k, const void* v,
+                                             void* o, sa2pp_run_report* report);
 /* Block the calling host thread until every call issued on `hp` has landed in host memory
  * (for callers without a CUDA stream of their own, e.g. a numpy binding). */
 SA2PP_API int sa2pp_host_pipeline_sync(sa2pp_host_pipeline* hp);

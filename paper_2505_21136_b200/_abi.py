@@ -22,7 +22,8 @@ EXPORTED = (
     "sa2pp_version", "sa2pp_last_error", "sa2pp_check_problem", "sa2pp_quant_sizes",
     "sa2pp_prepass", "sa2pp_attn_fwd", "sa2pp_sageattn", "sa2pp_set_debug_buffer",
     "sa2pp_set_trace_buffer", "sa2pp_host_pipeline_create", "sa2pp_host_pipeline_run",
-    "sa2pp_host_pipeline_sync", "sa2pp_host_pipeline_destroy",
+    "sa2pp_host_pipeline_sync", "sa2pp_host_pipeline_destroy", "sa2pp_host_pipeline_run_report",
+    "sa2pp_analytic_counts", "sa2pp_report_init",
 )
 
 
@@ -61,7 +62,14 @@ class Output(C.Structure):
 
 class Report(C.Structure):
     _fields_ = [("overflow_events", C.c_uint32), ("p_scale_min_bits", C.c_uint32),
-                ("p_scale_max_bits", C.c_uint32), ("reserved", C.c_uint32)]
+                ("p_scale_max_bits", C.c_uint32), ("reserved", C.c_uint32),
+                ("v_scale_min_bits", C.c_uint64), ("v_scale_max_bits", C.c_uint64)]
+
+
+class RunReport(C.Structure):  # sa2pp_run_report
+    _fields_ = [("overflow_events", C.c_uint64), ("fp16_to_fp32_conversions", C.c_uint64),
+                ("mma_invocations", C.c_uint64), ("p_scale_min", C.c_double), ("p_scale_max", C.c_double),
+                ("v_scale_min", C.c_double), ("v_scale_max", C.c_double)]
 
 
 _lib = None
@@ -91,6 +99,9 @@ def lib() -> C.CDLL:
         h.sa2pp_host_pipeline_run.argtypes = [C.c_void_p] * 6
         h.sa2pp_host_pipeline_sync.argtypes = [C.c_void_p]
         h.sa2pp_host_pipeline_destroy.argtypes = [C.c_void_p]
+        h.sa2pp_host_pipeline_run_report.argtypes = [C.c_void_p] * 5 + [P(RunReport)]
+        h.sa2pp_analytic_counts.argtypes = [P(Problem), P(C.c_uint64), P(C.c_uint64)]
+        h.sa2pp_report_init.argtypes = [C.c_void_p, C.c_void_p]
         for name in EXPORTED[2:]:
             getattr(h, name).restype = C.c_int
         _lib = h

@@ -175,7 +175,8 @@ class HostPipeline:
             self.device = torch.device("cuda", torch.cuda.current_device())
         prob = _problem(B, Hq, Hkv, N, D, causal=is_causal, pv_accum=pv_accum, sm_scale=sm_scale,
                         smoothing=kw.get("smooth", True), qk_bits=kw.get("qk_bits", 8),
-                        p_r=kw.get("p_r", 224.0), v_r=kw.get("v_r", 4.5))
+                        p_r=kw.get("p_r", 224.0), v_r=kw.get("v_r", 4.5), depth=kw.get("buffering_depth", 2),
+                        expect_overflow=kw.get("expect_overflow", False))
         self._h = A.C.c_void_p()
         with torch.cuda.device(self.device):
             A.check(A.lib().sa2pp_host_pipeline_create(C_ref(prob), _DT[dtype], chunks, depth, A.C.byref(self._h)))
@@ -190,6 +191,18 @@ class HostPipeline:
             A.check(A.lib().sa2pp_host_pipeline_run(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(),
                                                     out.data_ptr(), caller.cuda_stream))
         return out
+
+    def run_report(self, q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, out: torch.Tensor) -> A.RunReport:
+        """Blocking call with the instrumented kernels; returns the reference's RunReport counters
+        (sa2pp_host_pipeline_run_report) and leaves the output in `out`."""
+        for t, h in ((q, self.Hq), (k, self.Hkv), (v, self.Hkv), (out, self.Hq)):
+            if t.is_cuda or tuple(t.shape) != (self.B, h, self.N, self.D) or not t.is_contiguous() or t.dtype != self.dtype:
+                raise ValueError("HostPipeline takes contiguous [B, H, N, D] host tensors of its dtype")
+        rep = A.RunReport()
+        with torch.cuda.device(self.device):
+            A.check(A.lib().sa2pp_host_pipeline_run_report(self._h, q.data_ptr(), k.data_ptr(), v.data_ptr(),
+                                                           out.data_ptr(), A.C.byref(rep)))
+        return rep
 
     def close(self) -> None:
         if getattr(self, "_h", None) and self._h.value:
@@ -216,10 +229,20 @@ def sageattn_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, is_causal: 
 
 
 def new_report(device) -> torch.Tensor:
-    """Device RunReport buffer: overflow count, min/max delta_P as float bits (see sa2pp_report)."""
-    r = torch.zeros(4, dtype=torch.int32, device=device)
-    r[1] = 0x7F800000  # +inf bits for the running minimum
+    """Device RunReport buffer (sa2pp_report, 32 bytes): overflow count, min/max delta_P as float
+    bits, min/max delta_V as double bits."""
+    r = torch.zeros(8, dtype=torch.int32, device=device)
+    r[1] = 0x7F800000  # +inf bits for the running minimum of delta_P
+    r.view(torch.int64)[2] = 0x7FF0000000000000  # +inf bits (double) for the minimum of delta_V
     return r
+
+
+def read_report(rep: torch.Tensor) -> dict:
+    """Decode a device sa2pp_report (new_report) into the reference's field names."""
+    raw = rep.cpu().numpy()
+    u32, f32, f64 = raw.view(np.uint32), raw.view(np.float32), raw.view(np.float64)
+    return {"overflow_events": int(u32[0]), "p_scale_min": float(f32[1]), "p_scale_max": float(f32[2]),
+            "v_scale_min": float(f64[2]), "v_scale_max": float(f64[3])}
 
 
 # ----------------------------------------------------------------------------- reference mirror
@@ -293,20 +316,10 @@ def attention_quantized(q, k, v, config: AttentionConfig, *, device: str = "cuda
         buffering_depth=config.range.buffering_depth, expect_overflow=config.range.expect_overflow,
         return_quant=True, report=rep)
     torch.cuda.synchronize(tq.device)
-    r = rep.cpu().numpy().view(np.uint32)
-    vsc = qt.v_scale64
+    r = read_report(rep)
     conv, mma = _analytic_counts(config)
     o = out[0].double().cpu().numpy()
-    return RunReport(
-        output=o[0] if squeeze else o,
-        overflow_events=int(r[0]),
-        fp16_to_fp32_conversions=conv,
-        mma_invocations=mma,
-        p_scale_min=float(np.array([r[1]], dtype=np.uint32).view(np.float32)[0]),
-        p_scale_max=float(np.array([r[2]], dtype=np.uint32).view(np.float32)[0]),
-        v_scale_min=float(vsc.min()),
-        v_scale_max=float(vsc.max()),
-    )
+    return RunReport(output=o[0] if squeeze else o, fp16_to_fp32_conversions=conv, mma_invocations=mma, **r)
 
 
 def quantize(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, tensor_layout: str = "HND", *,

@@ -13,11 +13,13 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstring>
 #include <vector>
 
 #include "sa2pp_internal.h"
 
 struct sa2pp_host_pipeline {
+  sa2pp_problem full{};   // the whole call's problem (for the analytic RunReport counters)
   sa2pp_problem chunk{};  // one chunk's problem: batch 1, cu*group query heads, cu kv heads
   int dtype = 0, es = 2, group = 1, units = 0, cu = 1, n_chunks = 0, depth = 1, device = 0;
   size_t q_unit = 0, kv_unit = 0;  // bytes of one unit of Q (group heads) / of K or V (one head)
@@ -29,6 +31,7 @@ struct sa2pp_host_pipeline {
   };
   std::vector<Set> sets;
   void* mem = nullptr;
+  sa2pp_report* report = nullptr;  // device report shared by the chunks of a run_report call
   cudaStream_t h2d = nullptr, comp = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> ev_in, ev_comp, ev_out;
   cudaEvent_t done = nullptr;
@@ -90,6 +93,7 @@ int sa2pp_host_pipeline_create(const sa2pp_problem* prob, int dtype, int chunks,
   hp->depth = std::min(depth, hp->n_chunks);
   hp->kv_unit = static_cast<size_t>(prob->seq_len) * prob->head_dim * hp->es;
   hp->q_unit = hp->kv_unit * hp->group;
+  hp->full = *prob;
   hp->chunk = *prob;
   hp->chunk.batch = 1;
   hp->chunk.heads_q = hp->cu * hp->group;
@@ -105,7 +109,7 @@ int sa2pp_host_pipeline_create(const sa2pp_problem* prob, int dtype, int chunks,
                         qs.kv_meta, qs.kv_scale64, qs.bias, qs.bias_l2, qs.means};
   size_t per_set = 2 * round_up(hp->cu * hp->q_unit) + 2 * round_up(hp->cu * hp->kv_unit) + round_up(qs.workspace);
   for (size_t b : qsz) per_set += round_up(b);
-  cudaError_t e = cudaMalloc(&hp->mem, per_set * hp->depth);
+  cudaError_t e = cudaMalloc(&hp->mem, per_set * hp->depth + round_up(sizeof(sa2pp_report)));
   if (e != cudaSuccess) {
     release(hp);
     return sa2pp::set_error(SA2PP_ERR_CUDA, "host pipeline: cudaMalloc(%zu): %s", per_set * hp->depth,
@@ -137,6 +141,7 @@ int sa2pp_host_pipeline_create(const sa2pp_problem* prob, int dtype, int chunks,
     S.ws = take(qs.workspace);
     hp->sets.push_back(S);
   }
+  hp->report = reinterpret_cast<sa2pp_report*>(take(sizeof(sa2pp_report)));
   for (cudaStream_t* s : {&hp->h2d, &hp->comp, &hp->d2h})
     if ((e = cudaStreamCreateWithFlags(s, cudaStreamNonBlocking)) != cudaSuccess) break;
   for (auto* v : {&hp->ev_in, &hp->ev_comp, &hp->ev_out}) {
@@ -152,8 +157,12 @@ int sa2pp_host_pipeline_create(const sa2pp_problem* prob, int dtype, int chunks,
   return SA2PP_OK;
 }
 
-int sa2pp_host_pipeline_run(sa2pp_host_pipeline* hp, const void* q, const void* k, const void* v, void* o,
-                            void* cuda_stream) {
+}  // extern "C"
+
+namespace {
+
+int enqueue(sa2pp_host_pipeline* hp, const void* q, const void* k, const void* v, void* o, void* cuda_stream,
+            sa2pp_report* report) {
   if (!hp) return sa2pp::set_error(SA2PP_ERR_INVALID, "host pipeline handle is NULL");
   if (!q || !k || !v || !o) return sa2pp::set_error(SA2PP_ERR_INVALID, "q, k, v and o must be host pointers");
   DeviceGuard guard(hp->device);
@@ -192,7 +201,7 @@ int sa2pp_host_pipeline_run(sa2pp_host_pipeline* hp, const void* q, const void* 
     out.dtype = static_cast<sa2pp_dtype>(hp->dtype);
     out.o = S.o;
     for (int j = 0; j < 3; ++j) out.o_stride[j] = qst[j];
-    const int rc = sa2pp_sageattn(&pr, &in, &S.qt, S.ws, S.ws_bytes, &out, nullptr, hp->comp);
+    const int rc = sa2pp_sageattn(&pr, &in, &S.qt, S.ws, S.ws_bytes, &out, report, hp->comp);
     if (rc) return rc;
     e = cudaEventRecord(hp->ev_comp[s], hp->comp);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(hp->d2h, hp->ev_comp[s], 0);
@@ -203,6 +212,45 @@ int sa2pp_host_pipeline_run(sa2pp_host_pipeline* hp, const void* q, const void* 
   if (e == cudaSuccess) e = cudaEventRecord(hp->done, hp->d2h);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(static_cast<cudaStream_t>(cuda_stream), hp->done, 0);
   if (e != cudaSuccess) return sa2pp::set_error(SA2PP_ERR_CUDA, "host pipeline: %s", cudaGetErrorString(e));
+  return SA2PP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sa2pp_host_pipeline_run(sa2pp_host_pipeline* hp, const void* q, const void* k, const void* v, void* o,
+                            void* cuda_stream) {
+  return enqueue(hp, q, k, v, o, cuda_stream, nullptr);
+}
+
+int sa2pp_host_pipeline_run_report(sa2pp_host_pipeline* hp, const void* q, const void* k, const void* v, void* o,
+                                   sa2pp_run_report* report) {
+  if (!hp) return sa2pp::set_error(SA2PP_ERR_INVALID, "host pipeline handle is NULL");
+  if (!report) return sa2pp::set_error(SA2PP_ERR_INVALID, "report is NULL");
+  DeviceGuard guard(hp->device);
+  int rc = sa2pp_report_init(hp->report, hp->comp);  // ordered before every chunk's kernels
+  if (rc) return rc;
+  if ((rc = enqueue(hp, q, k, v, o, hp->comp, hp->report))) return rc;
+  if ((rc = sa2pp_host_pipeline_sync(hp))) return rc;
+  sa2pp_report r{};
+  cudaError_t e = cudaMemcpy(&r, hp->report, sizeof(r), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return sa2pp::set_error(SA2PP_ERR_CUDA, "host pipeline report: %s", cudaGetErrorString(e));
+  uint64_t conv = 0, mma = 0;
+  if ((rc = sa2pp_analytic_counts(&hp->full, &conv, &mma))) return rc;
+  float pmin, pmax;
+  double vmin, vmax;
+  std::memcpy(&pmin, &r.p_scale_min_bits, 4);
+  std::memcpy(&pmax, &r.p_scale_max_bits, 4);
+  std::memcpy(&vmin, &r.v_scale_min_bits, 8);
+  std::memcpy(&vmax, &r.v_scale_max_bits, 8);
+  report->overflow_events = r.overflow_events;
+  report->fp16_to_fp32_conversions = conv;
+  report->mma_invocations = mma;
+  report->p_scale_min = pmin;
+  report->p_scale_max = pmax;
+  report->v_scale_min = vmin;
+  report->v_scale_max = vmax;
   return SA2PP_OK;
 }
 

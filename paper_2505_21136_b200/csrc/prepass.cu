@@ -15,6 +15,7 @@
 //   quantize_kv    grid (nKB, B*Hkv)          one CTA per 64-key block (K codes, V^T codes, scales, bias)
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <algorithm>
 #include <cstdint>
 #include <type_traits>
 
@@ -811,6 +812,53 @@ cudaError_t launch_prepass(const PrepassLaunch& L, cudaStream_t st) {
     case SA2PP_BF16 * 1000 + 128: return launch_prepass_t<__nv_bfloat16, 128>(L, st);
     default: return cudaErrorInvalidValue;
   }
+}
+
+}  // namespace sa2pp
+
+// ------------------------------------------------------------------ run-report helpers
+namespace sa2pp {
+
+__global__ void report_init_kernel(sa2pp_report* r) {
+  r->overflow_events = 0u;
+  r->p_scale_min_bits = 0x7f800000u;
+  r->p_scale_max_bits = 0u;
+  r->reserved = 0u;
+  r->v_scale_min_bits = 0x7ff0000000000000ull;
+  r->v_scale_max_bits = 0ull;
+}
+
+// Positive doubles order like their bit patterns, so 64-bit integer atomics give FP64 min/max.
+__global__ void vscale_minmax_kernel(const double* __restrict__ s, int64_t blocks, int D, sa2pp_report* r) {
+  unsigned long long mn = 0x7ff0000000000000ull, mx = 0ull;
+  const int64_t n = blocks * D;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const unsigned long long b = __double_as_longlong(s[(i / D) * (1 + D) + 1 + i % D]);
+    mn = b < mn ? b : mn;
+    mx = b > mx ? b : mx;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long a = __shfl_xor_sync(0xffffffffu, mn, o), c = __shfl_xor_sync(0xffffffffu, mx, o);
+    mn = a < mn ? a : mn;
+    mx = c > mx ? c : mx;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(reinterpret_cast<unsigned long long*>(&r->v_scale_min_bits), mn);
+    atomicMax(reinterpret_cast<unsigned long long*>(&r->v_scale_max_bits), mx);
+  }
+}
+
+cudaError_t launch_report_init(sa2pp_report* r, cudaStream_t st) {
+  report_init_kernel<<<1, 1, 0, st>>>(r);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_vscale_minmax(const double* kv_scale64, int64_t blocks, int D, sa2pp_report* r, cudaStream_t st) {
+  const int64_t n = blocks * D;
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 1184));
+  vscale_minmax_kernel<<<grid, 256, 0, st>>>(kv_scale64, blocks, D, r);
+  return cudaGetLastError();
 }
 
 }  // namespace sa2pp

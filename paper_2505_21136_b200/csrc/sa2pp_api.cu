@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdarg>
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -82,6 +83,35 @@ int sa2pp_set_debug_buffer(void* dbg) {
 
 int sa2pp_set_trace_buffer(void* buf) {
   g_trace = static_cast<unsigned long long*>(buf);
+  return SA2PP_OK;
+}
+
+int sa2pp_analytic_counts(const sa2pp_problem* p, uint64_t* conversions, uint64_t* mma_invocations) {
+  int rc = sa2pp_check_problem(p);
+  if (rc) return rc;
+  if (!conversions || !mma_invocations) return fail(SA2PP_ERR_INVALID, "output pointers must be set");
+  // mma.py:67-86 as lpattn counts them per (query tile, visible key block): QK^T = rows*64 dot
+  // products of ceil(D/32) k=32 MMAs, PV = rows*D of 64/32; FP16 accumulation converts each
+  // output once per ceil(groups/depth) group sums (attention.py:282-303)
+  const int64_t N = p->seq_len, D = p->head_dim, n_kb = (N + 63) / 64;
+  uint64_t conv = 0, mma = 0;
+  for (int64_t i0 = 0; i0 < N; i0 += 128) {
+    const int64_t rows = std::min<int64_t>(128, N - i0);
+    const int64_t stop = std::min<int64_t>(i0 + 128, N);
+    const int64_t vis = p->causal ? std::min<int64_t>(n_kb, (stop + 63) / 64) : n_kb;
+    mma += vis * (rows * 64 * ((D + 31) / 32) + rows * D * 2);
+    if (p->pv_accum == SA2PP_ACC_F16) conv += vis * rows * D * ((2 + p->buffering_depth - 1) / p->buffering_depth);
+  }
+  const uint64_t heads = static_cast<uint64_t>(p->batch) * p->heads_q;
+  *conversions = conv * heads;
+  *mma_invocations = mma * heads;
+  return SA2PP_OK;
+}
+
+int sa2pp_report_init(sa2pp_report* r, void* stream) {
+  if (!r) return fail(SA2PP_ERR_INVALID, "report is NULL");
+  cudaError_t e = sa2pp::launch_report_init(r, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "report init");
   return SA2PP_OK;
 }
 
@@ -249,6 +279,11 @@ int sa2pp_attn_fwd(const sa2pp_problem* p, const sa2pp_quant* qt, const sa2pp_ou
   cudaError_t e = use_v4 && !depth1_f16 ? sa2pp::launch_attn(*p, P, *qt, static_cast<cudaStream_t>(stream))
                                                 : sa2pp::launch_attn_ws(*p, P, *qt, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
+  if (report != nullptr) {  // v_scale min/max over every (key block, channel) (attention.py:271-275)
+    e = sa2pp::launch_vscale_minmax(qt->kv_scale64, static_cast<int64_t>(p->batch) * p->heads_kv * d.n_kb, p->head_dim,
+                                    report, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "report launch");
+  }
   return SA2PP_OK;
 }
 

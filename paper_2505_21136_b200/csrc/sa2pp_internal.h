@@ -75,6 +75,9 @@ struct AttnParams {
 cudaError_t launch_prepass(const PrepassLaunch& L, cudaStream_t st);
 cudaError_t launch_attn(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st);
 cudaError_t launch_attn_ws(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st);
+cudaError_t launch_report_init(sa2pp_report* r, cudaStream_t st);
+// min/max of the FP64 V scales [blocks][1 + D] (column 0 is dK) into report->v_scale_{min,max}_bits
+cudaError_t launch_vscale_minmax(const double* kv_scale64, int64_t blocks, int D, sa2pp_report* r, cudaStream_t st);
 
 // 2-D uint8 TMA map (inner extent `inner` bytes, `rows` rows of `row_bytes`), box box_inner x box_rows.
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

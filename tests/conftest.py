@@ -27,6 +27,18 @@ def golden_cases() -> list[str]:
     return sorted(p.stem for p in GOLDEN.glob("attn_*.npz"))
 
 
+BASELINE_REF = ROOT / "baseline" / "_ref"
+
+
+def lpattn_path():
+    """Where the unmodified reference package can be imported from: the pip-installed copy in
+    baseline/_ref (travels to the GPU box) or the read-only source tree (build container)."""
+    for p in (BASELINE_REF, REF_SRC):
+        if (p / "lpattn" / "__init__.py").exists():
+            return p
+    return None
+
+
 def reference_available() -> bool:
     return (REF_SRC / "lpattn" / "__init__.py").exists()
 

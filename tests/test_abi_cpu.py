@@ -161,3 +161,31 @@ def test_integration_stub_is_valid_python_and_binds_declared_symbols():
     assert called and called <= set(declared_functions()), called - set(declared_functions())
     for name in re.findall(r"#.*?\b(sa2pp_[a-z_]+)\b", block):  # types named in comments exist too
         assert name in header, name
+
+
+def test_analytic_counts_c_abi_equals_python_mirror():
+    """sa2pp_analytic_counts (used by the host RunReport) equals the Python mirror of mma.py's
+    counting on ragged, causal, depth-1/2 and FP32-accumulator configurations."""
+    import ctypes
+    from paper_2505_21136_b200.api import _analytic_counts, _problem
+    for n, d, causal, depth, acc in ((100, 64, False, 2, "fp16"), (1000, 128, True, 1, "fp16"),
+                                     (17776 // 8, 64, False, 2, "fp32"), (257, 128, True, 2, "fp16")):
+        cfg = sa.AttentionConfig(seq_len=n, head_dim=d, num_heads=3, causal=causal, pv_accumulator=acc,
+                                 range=sa.RangeConfig(224.0, 4.5, depth) if acc == "fp16"
+                                 else sa.RangeConfig(448.0, 448.0, 1, expect_overflow=True))
+        prob = _problem(1, 3, 3, n, d, causal=causal, pv_accum=acc, depth=cfg.range.buffering_depth,
+                        p_r=cfg.range.p_r, v_r=cfg.range.v_r, expect_overflow=cfg.range.expect_overflow)
+        conv, mma = ctypes.c_uint64(), ctypes.c_uint64()
+        assert A.lib().sa2pp_analytic_counts(ctypes.byref(prob), ctypes.byref(conv), ctypes.byref(mma)) == A.SA2PP_OK
+        assert (conv.value, mma.value) == _analytic_counts(cfg), (n, d, causal, depth, acc)
+
+
+def test_sageattn_custom_op_fake_tensor_shapes():
+    """torch.ops.sa2pp.sageattn propagates shapes and dtypes under FakeTensorMode (no GPU needed)."""
+    import torch
+    from torch._subclasses.fake_tensor import FakeTensorMode
+    with FakeTensorMode():
+        q = torch.empty(2, 300, 8, 64, dtype=torch.float16, device="cuda")
+        k = torch.empty(2, 300, 2, 64, dtype=torch.float16, device="cuda")
+        o = torch.ops.sa2pp.sageattn(q, k, k, "NHD", False, 0.125)
+        assert o.shape == q.shape and o.dtype == q.dtype

@@ -406,3 +406,74 @@ def test_rejects_unsupported_inputs():
     k = torch.randn(1, 4, 64, 64, device="cuda")
     with pytest.raises(ValueError):
         sa.sageattn(q, k, k)  # 6 query heads over 4 KV heads
+
+
+def _integration_stub():
+    """Execute the reference-side binding exactly as INTEGRATION.md prints it, against this build
+    (the only substitution is the library path), with the unmodified lpattn importable."""
+    import re
+    import sys
+    from conftest import ROOT, lpattn_path
+    where = lpattn_path()
+    if where is None:
+        pytest.skip("lpattn (baseline/_ref or /root/reference) not available")
+    if str(where) not in sys.path:
+        sys.path.insert(0, str(where))
+    text = (ROOT / "INTEGRATION.md").read_text()
+    block = re.search(r"```python\n(# lpattn/_b200\.py.*?)```", text, re.S).group(1)
+    block = block.replace('C.CDLL("libsa2pp.so")', f'C.CDLL({str(sa._abi.LIB_PATH)!r})')
+    ns = {}
+    exec(compile(block, "INTEGRATION.md", "exec"), ns)
+    return ns
+
+
+def test_integration_stub_run_report_matches_reference_counters():
+    """The INTEGRATION.md binding (numpy in, numpy + RunReport out through
+    sa2pp_host_pipeline_run_report) against the unmodified reference on the same inputs: every
+    counter of lpattn's RunReport (attention.py:114-125), output within the parity bar."""
+    ns = _integration_stub()
+    import lpattn
+    rng = np.random.Generator(np.random.Philox(21))
+    H, N, D = 2, 320, 64
+    q, k, v = (rng.standard_normal((H, N, D)).astype(np.float32) for _ in range(3))
+    cfg = lpattn.AttentionConfig(seq_len=N, head_dim=D, num_heads=H, causal=True)
+    got = ns["attention_quantized"](q, k, v, cfg)
+    want = lpattn.attention_quantized(q, k, v, cfg)
+    assert got.fp16_to_fp32_conversions == want.fp16_to_fp32_conversions
+    assert got.mma_invocations == want.mma_invocations
+    assert got.overflow_events == want.overflow_events == 0
+    assert got.v_scale_min == want.v_scale_min and got.v_scale_max == want.v_scale_max
+    for a, b in ((got.p_scale_min, want.p_scale_min), (got.p_scale_max, want.p_scale_max)):
+        assert abs(a - b) <= 1e-6 * b, (a, b)  # the kernel forms delta_P in FP32
+    cos, l1, _ = sa.compare(want.output, got.output)
+    assert cos >= 0.9999 and l1 <= 1e-3, (cos, l1)
+
+
+def test_integration_stub_reports_fp16_overflow():
+    """(448, 448) on all-ones inputs through the numpy binding: the real FP16 accumulator overflows
+    and the host RunReport carries the events (the reference's CLI fails on unwaived overflow,
+    cli.py:219-221); delta_P and delta_V equal the device-path report."""
+    ns = _integration_stub()
+    import lpattn
+    ones = np.ones((1, 64, 64), dtype=np.float32)
+    cfg = lpattn.AttentionConfig(seq_len=64, head_dim=64, num_heads=1,
+                                 range=lpattn.RangeConfig(448.0, 448.0, 2, expect_overflow=True))
+    got = ns["attention_quantized"](ones, ones, ones, cfg)
+    dev = sa.attention_quantized(ones, ones, ones, sa.AttentionConfig(
+        seq_len=64, head_dim=64, range=sa.RangeConfig(448.0, 448.0, 2, expect_overflow=True)))
+    assert got.overflow_events > 0 and got.overflow_events == dev.overflow_events
+    assert (got.p_scale_min, got.p_scale_max) == (dev.p_scale_min, dev.p_scale_max)
+    assert (got.v_scale_min, got.v_scale_max) == (dev.v_scale_min, dev.v_scale_max)
+
+
+def test_torch_library_op():
+    """torch.ops.sa2pp.sageattn: schema and fake-tensor checks (torch.library.opcheck) and the same
+    bits as the Python entry point."""
+    g = torch.Generator(device="cuda").manual_seed(4)
+    q, k, v = (torch.randn(1, 4, 200, 128, device="cuda", generator=g).bfloat16() for _ in range(3))
+    torch.library.opcheck(torch.ops.sa2pp.sageattn.default, (q, k, v, "HND", True, None),
+                          test_utils=("test_schema", "test_faketensor"))
+    a = torch.ops.sa2pp.sageattn(q, k, v, "HND", True, None)
+    b = sa.sageattn(q, k, v, "HND", True, None)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
