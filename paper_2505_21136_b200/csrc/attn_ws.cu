@@ -550,17 +550,20 @@ __global__ void __launch_bounds__(256, 2)
         }
       }
       __syncwarp();
-      constexpr bool kPipe = SA2PP_WS_PIPE != 0 && ACC16 && !INSTR;
+      // the pipelined promotion is the production path; the instrumented build keeps it too unless a
+      // debug dump or the overflow count needs the chunked variant (so traces time the real code)
+      constexpr bool kPipeOk = SA2PP_WS_PIPE != 0 && ACC16;
+      const bool pipe = kPipeOk && (!INSTR || (!dbg && !want_overflow));
       const uint32_t pv_col = C::kColPV + pb * D;
       if (__any_sync(0xffffffffu, alpha != 1.0f)) {
-        if constexpr (kPipe) {
-          promote_pipe(pv_col, alpha, std::true_type{});
+        if (pipe) {
+          if constexpr (kPipeOk) promote_pipe(pv_col, alpha, std::true_type{});
         } else {
           promote_impl(j, pv_col, alpha, std::true_type{});
         }
       } else {
-        if constexpr (kPipe) {
-          promote_pipe(pv_col, alpha, std::false_type{});
+        if (pipe) {
+          if constexpr (kPipeOk) promote_pipe(pv_col, alpha, std::false_type{});
         } else {
           promote_impl(j, pv_col, alpha, std::false_type{});
         }
