@@ -50,6 +50,33 @@ __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) 
       : "memory");
 }
 
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Wait policy by template argument: MODE 0 = suspend-hint try_wait (mbar_wait_sleep), 1 = plain
+// try_wait loop (mbar_wait), >1 = plain try_wait polled with a fixed __nanosleep(MODE) in between.
+// The suspend-hint form compiles to TRYWAIT + NANOSLEEP.SYNCS + PHASECHK and wakes on barrier
+// traffic of the CTA, i.e. it re-polls every few cycles.
+template <int MODE>
+__device__ __forceinline__ void mbar_wait_mode(uint64_t* bar, uint32_t parity) {
+  if constexpr (MODE == 0) {
+    mbar_wait_sleep(bar, parity);
+  } else if constexpr (MODE == 1) {
+    mbar_wait(bar, parity);
+  } else {
+    while (!mbar_try(bar, parity)) __nanosleep(MODE);
+  }
+}
+
 // ------------------------------------------------------------------ TMA
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
