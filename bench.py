@@ -50,6 +50,7 @@ def parse():
                     help="BASELINE.json configs: kernel (configs[1], the headline), cogvideox, llama, longctx")
     ap.add_argument("--seq", type=int, default=None, help="override the sequence length")
     ap.add_argument("--causal", action="store_true", help="causal variant of the kernel workload")
+    ap.add_argument("--head-dim", type=int, default=None, choices=[64, 128], help="override the head dim")
     ap.add_argument("--pv-accum", choices=["fp16", "fp32"], default="fp16")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -64,6 +65,8 @@ def resolve(a):
     B, Hq, Hkv, N, D, causal = WORKLOADS[a.workload]
     if a.seq is not None:
         N = a.seq
+    if a.head_dim is not None:
+        D = a.head_dim
     if a.causal:
         causal = True
     a.batch, a.heads, a.kv_heads, a.seq, a.head_dim, a.causal = B, Hq, Hkv, N, D, causal
@@ -290,7 +293,11 @@ def run_ours(a):
     def attn():
         A.check(lib.sa2pp_attn_fwd(ctypes.byref(prob), ctypes.byref(qs), ctypes.byref(o), None, sp))
 
-    launches_per_step = 4  # channel_means, quantize_q, quantize_kv, attention
+    launches_per_step = 5  # channel_means, quantize_q, quantize_k, quantize_v, attention
+    # inputs + output smaller than twice the 126 MB L2: flush it between timed steps (a 512 MB write,
+    # outside the per-step events) so every step reads Q/K/V from HBM
+    resident = sum(t.numel() * t.element_size() for t in (q, k, v, out))
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if resident < 2 * (126 << 20) else None
 
     for _ in range(a.warmup):
         exchange_in()
@@ -310,6 +317,8 @@ def run_ours(a):
         t_end = torch.cuda.Event(enable_timing=True)
         t_start.record(stream)
         for e0, e1, e2 in ev:
+            if flush is not None:
+                flush.fill_(1)
             exchange_in()
             e0.record(stream)
             prepass()
@@ -322,6 +331,8 @@ def run_ours(a):
         if world > 1:
             dist.barrier()
     total_ms = t_start.elapsed_time(t_end)
+    if flush is not None:  # the flushes sit between the timed steps, not in them
+        total_ms = sum(e0.elapsed_time(e2) for e0, _, e2 in ev)
     attn_ms = statistics.mean(e1.elapsed_time(e2) for _, e1, e2 in ev)
     pre_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1, _ in ev)
     if world > 1:
@@ -389,11 +400,12 @@ def run_ours(a):
         "config": {"workload": workload_name(a), "batch": B, "heads": H, "kv_heads": Hkv, "seq_len": N,
                    "head_dim": D, "causal": a.causal, "pv_accum": a.pv_accum,
                    "parallelism": (f"ulysses x{world}" if ulysses else f"bh-shard x{world}"),
-                   "l2": "inputs larger than L2 (%.0f MB bf16 Q/K/V per GPU)" % (
+                   "l2": ("L2 flushed between steps (512 MB write outside the step events); %.0f MB bf16 Q/K/V"
+                          if flush is not None else "inputs larger than L2 (%.0f MB bf16 Q/K/V per GPU)") % (
                        sum(t.numel() for t in (q, k, v)) * 2 / 1e6)},
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": fp8_peak, "unit": "TFLOP/s",
                      "frac": achieved / fp8_peak, "traffic": read_traffic(workload_name(a)),
-                     "kernel": "attn_fwd_kernel", "ops_per_launch": attn_ops_per_launch,
+                     "kernel": "attn_ws_kernel", "ops_per_launch": attn_ops_per_launch,
                      "ms_per_launch": attn_ms, "peak_source": f"2 x bf16 {bf16_peak} ({peak_src})",
                      "frac_of_nominal_4500": achieved / 4500.0,
                      "fp8_cublas_measured_tflops": read_fp8_measured()},

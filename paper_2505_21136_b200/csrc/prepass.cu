@@ -12,7 +12,8 @@
 // Kernels:
 //   channel_means  grid (B*(Hq+Hkv))          sequential FP64 channel sums in token order -> mean
 //   quantize_q     grid (nQT, B*Hq)           one CTA per 128-row query tile
-//   quantize_kv    grid (nKB, B*Hkv)          one CTA per 64-key block (K codes, V^T codes, scales, bias)
+//   quantize_k     grid (nKB, B*Hkv)          one CTA per 64-key block (K codes, dK, bias)
+//   quantize_v     grid (nKB, B*Hkv)          one CTA per 64-key block (V^T codes, dV)
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <algorithm>
@@ -448,42 +449,65 @@ __global__ void __launch_bounds__(256, 2) quantize_q_kernel(InView qv, int Hq, i
   }
 }
 
-// ------------------------------------------------------------------ pass 3: K/V blocks
-// One CTA (256 threads) per 64-key block of one (b, hkv).  Thread (rg, c8) holds channels
-// [8*c8, 8*c8+8) of the RT consecutive keys [rg*RT, rg*RT+RT) of both K and V in registers, so the
-// block is read from HBM exactly once and every output is produced from registers:
-//   k_codes  [B, Hkv, Np, D]          int8, 8-byte stores straight from registers
-//   v_codes  [B, Hkv, D, Np]          E4M3, transposed through a swizzled 64-byte-per-channel smem tile
-//   kv_meta  [B, Hkv, nKB, 4 + D]     f32 {dK, 0, 0, 0, dV[0..D)}
-//   bias     [B, Hq, Np]              f32 q_mean . Ks_j ; bias_l2 = bias * sm_scale * log2(e)
+// ------------------------------------------------------------------ pass 3: K blocks and V blocks
+// Two kernels, one CTA (256 threads) per 64-key block of one (b, hkv) each.  Thread (rg, c8) holds
+// channels [8*c8, 8*c8+8) of the RT consecutive keys [rg*RT, rg*RT+RT) in registers, so every block
+// is read from HBM exactly once and every output is produced from registers:
+//   quantize_k:  k_codes [B, Hkv, Np, D] int8 (8-byte stores), kv_meta dK, bias / bias_l2 [B, Hq, Np]
+//                (b_j = q_mean . Ks_j for every query head of the GQA group)
+//   quantize_v:  v_codes [B, Hkv, D, Np] E4M3 (transposed through a swizzled 64-byte-per-channel smem
+//                tile), kv_meta dV[0..D)
 // Per-channel statistics (K min/max, V |max|) are reduced across the row groups with shuffles and
-// across warps through shared memory; the block scalars need two CTA barriers, the transpose a third.
-template <typename T, int D>
-__host__ __device__ constexpr int kv_smem_bytes() {
-  return 3 * 8 * D * 4 + D * 64 + D * 8 + D * 4 + 64;
+// across warps through shared memory.  Splitting K from V halves the live registers, so three CTAs
+// share an SM instead of two (the single K+V kernel stalled on its three CTA barriers at two CTAs/SM).
+// three-input FMNMX3 (sm_100)
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float min3f(float a, float b, float c) {
+  float d;
+  asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InView v_in, int Hq, int Hkv, int N, int Np,
-                                                             int n_kb, int qmax, double v_r, int smoothing,
-                                                             double sm_scale_log2, const double* __restrict__ means,
-                                                             int Ht, int8_t* __restrict__ k_codes,
-                                                             uint8_t* __restrict__ v_codes, float* __restrict__ kv_meta,
-                                                             double* __restrict__ kv_scale64, float* __restrict__ bias,
-                                                             float* __restrict__ bias_l2) {
-  constexpr int LPR = D / 8;         // lanes per key row
-  constexpr int RPP = 256 / LPR;     // row groups per CTA
-  constexpr int RT = 64 / RPP;       // consecutive keys per thread (4 for D=128, 2 for D=64)
-  constexpr int UPR = 64 / RT;       // RT-byte units per 64-key V^T row
-  constexpr int NW = sizeof(T) == 4 ? 2 : 1;  // 16-byte loads per 8 channels
-  extern __shared__ __align__(16) unsigned char kv_smem[];
-  float* s_kmn = reinterpret_cast<float*>(kv_smem);  // [8 warps][D]
-  float* s_kmx = s_kmn + 8 * D;
-  float* s_vmx = s_kmx + 8 * D;
-  uint8_t* s_vt = reinterpret_cast<uint8_t*>(s_vmx + 8 * D);    // [D][64] swizzled E4M3 codes
-  double* s_vsc = reinterpret_cast<double*>(s_vt + D * 64);    // [D]
-  float* s_vinv = reinterpret_cast<float*>(s_vsc + D);         // [D]
-  double* s_red = reinterpret_cast<double*>(s_vinv + D);       // [4] amax, [4] |mu| max
+struct KvGeom {
+  static constexpr int LPR = D / 8;                     // lanes per key row
+  static constexpr int RPP = 256 / LPR;                 // row groups per CTA
+  static constexpr int RT = 64 / RPP;                   // consecutive keys per thread (4 at D=128, 2 at D=64)
+  static constexpr int UPR = 64 / RT;                   // RT-byte units per 64-key V^T row
+  static constexpr int NW = sizeof(T) == 4 ? 2 : 1;     // 16-byte loads per 8 channels
+};
+
+template <typename T, int D>
+__device__ __forceinline__ void load_rows(const InView& in, int b, int h, int n0, int rg, int c0, int rows,
+                                          KvTile<T> (&x)[KvGeom<T, D>::RT]) {
+  using G = KvGeom<T, D>;
+#pragma unroll
+  for (int rr = 0; rr < G::RT; ++rr) {
+    const int r = rg * G::RT + rr;
+#pragma unroll
+    for (int u = 0; u < G::NW; ++u) {
+      uint4 v4 = make_uint4(0, 0, 0, 0);
+      if (r < rows) v4 = __ldcs(reinterpret_cast<const uint4*>(row_ptr<T>(in, b, h, n0 + r) + c0) + u);
+      x[rr].w[4 * u] = v4.x; x[rr].w[4 * u + 1] = v4.y; x[rr].w[4 * u + 2] = v4.z; x[rr].w[4 * u + 3] = v4.w;
+    }
+  }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256, 3) quantize_k_kernel(InView kv_in, int Hq, int Hkv, int N, int Np, int n_kb,
+                                                            int qmax, int smoothing, double sm_scale_log2,
+                                                            const double* __restrict__ means, int Ht,
+                                                            int8_t* __restrict__ k_codes, float* __restrict__ kv_meta,
+                                                            double* __restrict__ kv_scale64, float* __restrict__ bias,
+                                                            float* __restrict__ bias_l2) {
+  using G = KvGeom<T, D>;
+  constexpr int LPR = G::LPR, RT = G::RT;
+  __shared__ float s_kmn[8 * D], s_kmx[8 * D];
+  __shared__ double s_red[8];
   const int kb = blockIdx.x;
   const int bh = blockIdx.y;
   const int b = bh / Hkv, h = bh % Hkv;
@@ -493,42 +517,43 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InVie
   const int c8 = tid % LPR, rg = tid / LPR;
   const int c0 = c8 * 8;
 
-  // ---- load: RT rows x 8 channels of K and V (rows past N are zero: padding after smoothing)
-  KvTile<T> kt[RT], vt[RT];
-#pragma unroll
-  for (int rr = 0; rr < RT; ++rr) {
-    const int r = rg * RT + rr;
-#pragma unroll
-    for (int u = 0; u < NW; ++u) {
-      uint4 kx = make_uint4(0, 0, 0, 0), vx = make_uint4(0, 0, 0, 0);
-      if (r < rows) {
-        kx = __ldcs(reinterpret_cast<const uint4*>(row_ptr<T>(kv_in, b, h, n0 + r) + c0) + u);
-        vx = __ldcs(reinterpret_cast<const uint4*>(row_ptr<T>(v_in, b, h, n0 + r) + c0) + u);
-      }
-      kt[rr].w[4 * u] = kx.x; kt[rr].w[4 * u + 1] = kx.y; kt[rr].w[4 * u + 2] = kx.z; kt[rr].w[4 * u + 3] = kx.w;
-      vt[rr].w[4 * u] = vx.x; vt[rr].w[4 * u + 1] = vx.y; vt[rr].w[4 * u + 2] = vx.z; vt[rr].w[4 * u + 3] = vx.w;
-    }
-  }
+  KvTile<T> kt[RT];  // rows past N are zero (padding after smoothing)
+  load_rows<T, D>(kv_in, b, h, n0, rg, c0, rows, kt);
   const double* kmu_g = means + (static_cast<int64_t>(b) * Ht + Hq + h) * D;
 
-  // ---- per-channel statistics over the block's valid rows
+  // ---- per-channel min/max over the block's valid rows
   {
-    float mn[8], mx[8], va[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      mn[i] = INFINITY;
-      mx[i] = -INFINITY;
-      va[i] = 0.0f;
-    }
-#pragma unroll
-    for (int rr = 0; rr < RT; ++rr) {
-      const bool ok = rg * RT + rr < rows;
+    float mn[8], mx[8];
+    if (rows == 64) {  // every block but a ragged last one: no validity selects
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float x = kt[rr].get(i);
-        mn[i] = fminf(mn[i], ok ? x : INFINITY);
-        mx[i] = fmaxf(mx[i], ok ? x : -INFINITY);
-        va[i] = fmaxf(va[i], fabsf(vt[rr].get(i)));
+        mn[i] = kt[0].get(i);
+        mx[i] = mn[i];
+      }
+#pragma unroll
+      for (int rr = 1; rr < RT; rr += 2) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float x1 = kt[rr].get(i), x2 = rr + 1 < RT ? kt[rr + 1].get(i) : x1;
+          mn[i] = min3f(mn[i], x1, x2);
+          mx[i] = max3f(mx[i], x1, x2);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        mn[i] = INFINITY;
+        mx[i] = -INFINITY;
+      }
+#pragma unroll
+      for (int rr = 0; rr < RT; ++rr) {
+        const bool ok = rg * RT + rr < rows;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float x = kt[rr].get(i);
+          mn[i] = fminf(mn[i], ok ? x : INFINITY);
+          mx[i] = fmaxf(mx[i], ok ? x : -INFINITY);
+        }
       }
     }
 #pragma unroll
@@ -537,46 +562,34 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InVie
       for (int i = 0; i < 8; ++i) {
         mn[i] = fminf(mn[i], __shfl_xor_sync(0xffffffffu, mn[i], o));
         mx[i] = fmaxf(mx[i], __shfl_xor_sync(0xffffffffu, mx[i], o));
-        va[i] = fmaxf(va[i], __shfl_xor_sync(0xffffffffu, va[i], o));
       }
     }
     if (lane < LPR) {
       float* d0 = s_kmn + warp * D + c0;
       float* d1 = s_kmx + warp * D + c0;
-      float* d2 = s_vmx + warp * D + c0;
       *reinterpret_cast<float4*>(d0) = make_float4(mn[0], mn[1], mn[2], mn[3]);
       *reinterpret_cast<float4*>(d0 + 4) = make_float4(mn[4], mn[5], mn[6], mn[7]);
       *reinterpret_cast<float4*>(d1) = make_float4(mx[0], mx[1], mx[2], mx[3]);
       *reinterpret_cast<float4*>(d1 + 4) = make_float4(mx[4], mx[5], mx[6], mx[7]);
-      *reinterpret_cast<float4*>(d2) = make_float4(va[0], va[1], va[2], va[3]);
-      *reinterpret_cast<float4*>(d2 + 4) = make_float4(va[4], va[5], va[6], va[7]);
     }
   }
   __syncthreads();
 
-  // ---- channel scalars: K smoothed amax (quantization.py:151-160; fl64(k - mu) is monotone in k, so
-  //      the channel min/max give the element-wise FP64 max), V scale (quantization.py:178-188)
+  // ---- smoothed amax (quantization.py:151-160): fl64(k - mu) is monotone in k, so the channel
+  //      min/max give the element-wise FP64 max
   float* meta = kv_meta + (static_cast<int64_t>(bh) * n_kb + kb) * (4 + D);
   double* sc64 = kv_scale64 + (static_cast<int64_t>(bh) * n_kb + kb) * (1 + D);
   if (tid < D) {
-    float mn = INFINITY, mx = -INFINITY, va = 0.0f;
+    float mn = INFINITY, mx = -INFINITY;
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
       mn = fminf(mn, s_kmn[w * D + tid]);
       mx = fmaxf(mx, s_kmx[w * D + tid]);
-      va = fmaxf(va, s_vmx[w * D + tid]);
     }
     const double mu = kmu_g[tid];
     double amax = 0.0;
     if (mx >= mn) amax = fmax(fabs(static_cast<double>(mx) - mu), fabs(static_cast<double>(mn) - mu));
     double mumax = fabs(mu);
-    const double sc = va > 0.0f ? static_cast<double>(va) / v_r : 1.0;
-    s_vsc[tid] = sc;
-    // a channel whose block max is below 2^-100 (its f32 reciprocal may overflow, its quotients may
-    // be subnormal) is encoded from the FP64 quotients; NaN marks it for the exact path below
-    s_vinv[tid] = (va > 0.0f && va < 0x1p-100f) ? __int_as_float(0x7fffffff) : static_cast<float>(1.0 / sc);
-    meta[4 + tid] = static_cast<float>(sc);
-    sc64[1 + tid] = sc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
@@ -646,6 +659,119 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InVie
     }
   }
 
+  // ---- bias for every query head sharing this KV head: b_j = q_mean . Ks_j (attention.py:288-289),
+  //      FP64 over this thread's 8 channels, then a butterfly over the LPR lanes of the row
+  {
+    const int group = Hq / Hkv;
+    for (int g = 0; g < group; ++g) {
+      const int hq = h * group + g;
+      double acc[RT];
+#pragma unroll
+      for (int rr = 0; rr < RT; ++rr) acc[rr] = 0.0;
+      if (smoothing) {
+        const double* qm_g = means + (static_cast<int64_t>(b) * Ht + hq) * D + c0;
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          const double2 q2 = *reinterpret_cast<const double2*>(qm_g + i);
+          const double2 m2 = *reinterpret_cast<const double2*>(kmu_g + c0 + i);  // L1-resident
+#pragma unroll
+          for (int rr = 0; rr < RT; ++rr) {
+            acc[rr] = fma(q2.x, static_cast<double>(kt[rr].get(i)) - m2.x, acc[rr]);
+            acc[rr] = fma(q2.y, static_cast<double>(kt[rr].get(i + 1)) - m2.y, acc[rr]);
+          }
+        }
+#pragma unroll
+        for (int o = 1; o < LPR; o <<= 1) {
+#pragma unroll
+          for (int rr = 0; rr < RT; ++rr) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
+        }
+      }
+      if (c8 < RT) {
+        const int r = rg * RT + c8;
+        double a = acc[0];
+#pragma unroll
+        for (int rr = 1; rr < RT; ++rr)
+          if (c8 == rr) a = acc[rr];
+        if (r >= rows) a = 0.0;
+        const int64_t o = (static_cast<int64_t>(b) * Hq + hq) * Np + n0 + r;
+        bias[o] = static_cast<float>(a);
+        bias_l2[o] = static_cast<float>(a * sm_scale_log2);
+      }
+    }
+  }
+}
+
+template <typename T, int D>
+__host__ __device__ constexpr int v_smem_bytes() {
+  return 8 * D * 4 + D * 64 + D * 8 + D * 4;
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256, 3) quantize_v_kernel(InView v_in, int Hkv, int N, int Np, int n_kb, double v_r,
+                                                            uint8_t* __restrict__ v_codes, float* __restrict__ kv_meta,
+                                                            double* __restrict__ kv_scale64) {
+  using G = KvGeom<T, D>;
+  constexpr int LPR = G::LPR, RT = G::RT, UPR = G::UPR;
+  extern __shared__ __align__(16) unsigned char v_smem[];
+  float* s_vmx = reinterpret_cast<float*>(v_smem);              // [8 warps][D]
+  uint8_t* s_vt = reinterpret_cast<uint8_t*>(s_vmx + 8 * D);    // [D][64] swizzled E4M3 codes
+  double* s_vsc = reinterpret_cast<double*>(s_vt + D * 64);     // [D]
+  float* s_vinv = reinterpret_cast<float*>(s_vsc + D);          // [D]
+  const int kb = blockIdx.x;
+  const int bh = blockIdx.y;
+  const int b = bh / Hkv, h = bh % Hkv;
+  const int n0 = kb * 64;
+  const int rows = min(64, N - n0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int c8 = tid % LPR, rg = tid / LPR;
+  const int c0 = c8 * 8;
+
+  KvTile<T> vt[RT];  // rows past N are zero (the reference pads V with zeros)
+  load_rows<T, D>(v_in, b, h, n0, rg, c0, rows, vt);
+
+  // ---- per-channel |max| over the block (zero rows do not change it)
+  {
+    float va[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) va[i] = fabsf(vt[0].get(i));
+#pragma unroll
+    for (int rr = 1; rr < RT; rr += 2) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float x1 = fabsf(vt[rr].get(i)), x2 = rr + 1 < RT ? fabsf(vt[rr + 1].get(i)) : x1;
+        va[i] = max3f(va[i], x1, x2);
+      }
+    }
+#pragma unroll
+    for (int o = LPR; o < 32; o <<= 1) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) va[i] = fmaxf(va[i], __shfl_xor_sync(0xffffffffu, va[i], o));
+    }
+    if (lane < LPR) {
+      float* d2 = s_vmx + warp * D + c0;
+      *reinterpret_cast<float4*>(d2) = make_float4(va[0], va[1], va[2], va[3]);
+      *reinterpret_cast<float4*>(d2 + 4) = make_float4(va[4], va[5], va[6], va[7]);
+    }
+  }
+  __syncthreads();
+
+  // ---- V scale per (block, channel) (quantization.py:178-188)
+  float* meta = kv_meta + (static_cast<int64_t>(bh) * n_kb + kb) * (4 + D);
+  double* sc64 = kv_scale64 + (static_cast<int64_t>(bh) * n_kb + kb) * (1 + D);
+  if (tid < D) {
+    float va = 0.0f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) va = fmaxf(va, s_vmx[w * D + tid]);
+    const double sc = va > 0.0f ? static_cast<double>(va) / v_r : 1.0;
+    s_vsc[tid] = sc;
+    // a channel whose block max is below 2^-100 (its f32 reciprocal may overflow, its quotients may
+    // be subnormal) is encoded from the FP64 quotients; NaN marks it for the exact path below
+    s_vinv[tid] = (va > 0.0f && va < 0x1p-100f) ? __int_as_float(0x7fffffff) : static_cast<float>(1.0 / sc);
+    meta[4 + tid] = static_cast<float>(sc);
+    sc64[1 + tid] = sc;
+  }
+  __syncthreads();
+
   // ---- V codes (E4M3, RNE, satfinite): tie test = the codes of q*(1 -+ 2^-20) differ, which brackets
   //      the exact FP64 quotient; flagged elements are re-encoded from it.  Codes go to a transposed
   //      smem tile: RT-byte unit (channel c, keys [rg*RT, +RT)) at unit index rg ^ swz(c8).
@@ -688,53 +814,6 @@ __global__ void __launch_bounds__(256, 2) quantize_kv_kernel(InView kv_in, InVie
       const int i = bit / RT, rr = bit % RT, c = c0 + i;
       const float x = to_f32<T>(row_ptr<T>(v_in, b, h, n0 + rg * RT + rr)[c]);
       s_vt[c * 64 + (rg ^ swz) * RT + rr] = v_code_exact(x, s_vsc[c]);
-    }
-  }
-
-  // ---- bias for every query head sharing this KV head: b_j = q_mean . Ks_j (attention.py:288-289),
-  //      FP64 over this thread's 8 channels, then a butterfly over the LPR lanes of the row
-  {
-    const int group = Hq / Hkv;
-    double km[8];
-#pragma unroll
-    for (int i = 0; i < 8; i += 2) {
-      const double2 m2 = *reinterpret_cast<const double2*>(kmu_g + c0 + i);
-      km[i] = m2.x;
-      km[i + 1] = m2.y;
-    }
-    for (int g = 0; g < group; ++g) {
-      const int hq = h * group + g;
-      double acc[RT];
-#pragma unroll
-      for (int rr = 0; rr < RT; ++rr) acc[rr] = 0.0;
-      if (smoothing) {
-        const double* qm_g = means + (static_cast<int64_t>(b) * Ht + hq) * D + c0;
-#pragma unroll
-        for (int i = 0; i < 8; i += 2) {
-          const double2 q2 = *reinterpret_cast<const double2*>(qm_g + i);
-#pragma unroll
-          for (int rr = 0; rr < RT; ++rr) {
-            acc[rr] = fma(q2.x, static_cast<double>(kt[rr].get(i)) - km[i], acc[rr]);
-            acc[rr] = fma(q2.y, static_cast<double>(kt[rr].get(i + 1)) - km[i + 1], acc[rr]);
-          }
-        }
-#pragma unroll
-        for (int o = 1; o < LPR; o <<= 1) {
-#pragma unroll
-          for (int rr = 0; rr < RT; ++rr) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
-        }
-      }
-      if (c8 < RT) {
-        const int r = rg * RT + c8;
-        double a = acc[0];
-#pragma unroll
-        for (int rr = 1; rr < RT; ++rr)
-          if (c8 == rr) a = acc[rr];
-        if (r >= rows) a = 0.0;
-        const int64_t o = (static_cast<int64_t>(b) * Hq + hq) * Np + n0 + r;
-        bias[o] = static_cast<float>(a);
-        bias_l2[o] = static_cast<float>(a * sm_scale_log2);
-      }
     }
   }
 
@@ -790,15 +869,16 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
                                                        L.q_codes, L.q_scale, L.q_scale64);
   }
   dim3 gk(L.n_kb, L.B * L.Hkv);
-  constexpr int kv_smem = kv_smem_bytes<T, D>();
-  static PerDevice kv_once;
-  cudaError_t e = kv_once.run([&](std::atomic<int>&) {
-    return cudaFuncSetAttribute(quantize_kv_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kv_smem);
+  quantize_k_kernel<T, D><<<gk, 256, 0, st>>>(kv, L.Hq, L.Hkv, L.N, L.Np, L.n_kb, L.qmax, L.smoothing, L.sm_scale_log2,
+                                              L.means, Ht, L.k_codes, L.kv_meta, L.kv_scale64, L.bias, L.bias_l2);
+  constexpr int v_smem = v_smem_bytes<T, D>();
+  static PerDevice v_once;
+  cudaError_t e = v_once.run([&](std::atomic<int>&) {
+    return cudaFuncSetAttribute(quantize_v_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, v_smem);
   });
   if (e != cudaSuccess) return e;
-  quantize_kv_kernel<T, D><<<gk, 256, kv_smem, st>>>(kv, vv, L.Hq, L.Hkv, L.N, L.Np, L.n_kb, L.qmax, L.v_r, L.smoothing,
-                                               L.sm_scale_log2, L.means, Ht, L.k_codes, L.v_codes, L.kv_meta,
-                                               L.kv_scale64, L.bias, L.bias_l2);
+  quantize_v_kernel<T, D><<<gk, 256, v_smem, st>>>(vv, L.Hkv, L.N, L.Np, L.n_kb, L.v_r, L.v_codes, L.kv_meta,
+                                                   L.kv_scale64);
   return cudaGetLastError();
 }
 
