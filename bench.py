@@ -7,9 +7,10 @@
 Workload (BASELINE.json configs[1], the headline): kernel bench, batch 4, 32 heads,
 head_dim 128, seq 16384, non-causal, bf16 Q/K/V (synthetic N(0,1)).  A step is one
 sageattn forward (prepass + attention kernel) over the whole batch.  Metric: attention
-TOPS = 4*B*H*N^2*D (x0.5 causal) / time.  Multi-GPU: the 128 (batch, head) units are
-sharded across ranks with no data-path collective (strong scaling); value = all ranks'
-ops / max-over-ranks device time.  Rank 0 prints ONE JSON line.
+TOPS = 4*B*H*N^2*D (x0.5 causal) / time.  Multi-GPU: the 128-row query tiles of all
+(batch, head)s are split contiguously across ranks (parallel.TilePlan, balanced to one tile) with
+no data-path collective (strong scaling); the long-context config uses the Ulysses all-to-all.
+value = all ranks' ops / max-over-ranks device time.  Rank 0 prints ONE JSON line.
 
 --impl reference times the reference's CPU path -- the unmodified lpattn.attention_quantized,
 pip-installed into baseline/_ref (falls back to the oracle port in oracle/sage_cpu.py if that
@@ -251,8 +252,11 @@ def run_ours(a):
         # sequence-sharded input [1, N/P, H, D] per rank; all-to-all to [1, N, H/P, D] and back
         Ul, Nl = H // world, N // world
     else:
-        # (batch, head) units sharded across ranks (GQA groups kept whole); no data-path collective
-        Ul, Nl = len(parallel.shard_units(B, H, world, rank, group)), N
+        # 128-row query tiles of all (batch, head)s sharded contiguously across ranks (balanced to one
+        # tile); each rank quantizes the heads (whole GQA groups) its range touches; no collective
+        plan = parallel.tile_plan(B, H, Hkv, N, world, rank)
+        Ul, Nl = plan.local_heads, N
+        u0, u1 = plan.local_units
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     rnd = lambda *shape: torch.randn(*shape, device=dev, generator=gen, dtype=torch.float32).bfloat16()  # noqa: E731
     if ulysses:
@@ -291,7 +295,11 @@ def run_ours(a):
                                   qt.workspace.data_ptr(), qt.workspace.numel(), sp))
 
     def attn():
-        A.check(lib.sa2pp_attn_fwd(ctypes.byref(prob), ctypes.byref(qs), ctypes.byref(o), None, sp))
+        if ulysses:
+            A.check(lib.sa2pp_attn_fwd(ctypes.byref(prob), ctypes.byref(qs), ctypes.byref(o), None, sp))
+        else:
+            A.check(lib.sa2pp_attn_fwd_units(ctypes.byref(prob), ctypes.byref(qs), ctypes.byref(o), None, u0, u1 - u0,
+                                             sp))
 
     launches_per_step = 5  # channel_means, quantize_q, quantize_k, quantize_v, attention
     # inputs + output smaller than twice the 126 MB L2: flush it between timed steps (a 512 MB write,
@@ -389,7 +397,8 @@ def run_ours(a):
 
     bf16_peak, peak_src = read_peaks()
     fp8_peak = 2.0 * bf16_peak  # dense FP8/INT8 tensor rate is 2x dense BF16 on B200
-    attn_ops_per_launch = ops_of(1, Ul, N, D, a.causal)
+    # the attention launch of rank 0: its share of the query tiles (all of them at world 1)
+    attn_ops_per_launch = ops_of(B, H, N, D, a.causal) * ((u1 - u0) / plan.total_units if not ulysses else 1.0 / world)
     achieved = attn_ops_per_launch / (attn_ms * 1e-3) / 1e12
     line = {
         "metric": metric_name(), "value": value, "unit": "TOPS", "n_gpus": world,
@@ -399,7 +408,7 @@ def run_ours(a):
         "data": "synthetic N(0,1) bf16 Q/K/V",
         "config": {"workload": workload_name(a), "batch": B, "heads": H, "kv_heads": Hkv, "seq_len": N,
                    "head_dim": D, "causal": a.causal, "pv_accum": a.pv_accum,
-                   "parallelism": (f"ulysses x{world}" if ulysses else f"bh-shard x{world}"),
+                   "parallelism": (f"ulysses x{world}" if ulysses else f"q-tile shard x{world}"),
                    "l2": ("L2 flushed between steps (512 MB write outside the step events); %.0f MB bf16 Q/K/V"
                           if flush is not None else "inputs larger than L2 (%.0f MB bf16 Q/K/V per GPU)") % (
                        sum(t.numel() for t in (q, k, v)) * 2 / 1e6)},

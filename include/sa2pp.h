@@ -168,6 +168,14 @@ SA2PP_API int sa2pp_attn_fwd(const sa2pp_problem* prob, const sa2pp_quant* qt, c
                    sa2pp_report* report, void* cuda_stream);
 
 /* Prepass + attention in one call: the attention_quantized / sageattn operator. */
+/* sa2pp_attn_fwd over a contiguous range of query tiles only: units u in [unit_begin,
+ * unit_begin + unit_count) of the flattened u = (b * heads_q + h) * ceil(N/128) + tile index; output
+ * rows of other tiles are left untouched.  The quantized tensors must cover every head the range
+ * touches (sa2pp_prepass of the whole problem).  This is the (b, h, q-tile) sharding unit of the
+ * multi-GPU layout; sa2pp_attn_fwd is the full range. */
+SA2PP_API int sa2pp_attn_fwd_units(const sa2pp_problem* prob, const sa2pp_quant* qt, const sa2pp_output* out,
+                                   sa2pp_report* report, int64_t unit_begin, int64_t unit_count, void* stream);
+
 SA2PP_API int sa2pp_sageattn(const sa2pp_problem* prob, const sa2pp_inputs* in, const sa2pp_quant* qt, void* workspace,
                    size_t workspace_bytes, const sa2pp_output* out, sa2pp_report* report, void* cuda_stream);
 

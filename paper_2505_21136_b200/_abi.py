@@ -23,7 +23,7 @@ EXPORTED = (
     "sa2pp_prepass", "sa2pp_attn_fwd", "sa2pp_sageattn", "sa2pp_set_debug_buffer",
     "sa2pp_set_trace_buffer", "sa2pp_host_pipeline_create", "sa2pp_host_pipeline_run",
     "sa2pp_host_pipeline_sync", "sa2pp_host_pipeline_destroy", "sa2pp_host_pipeline_run_report",
-    "sa2pp_analytic_counts", "sa2pp_report_init",
+    "sa2pp_analytic_counts", "sa2pp_report_init", "sa2pp_attn_fwd_units",
 )
 
 
@@ -91,6 +91,8 @@ def lib() -> C.CDLL:
         h.sa2pp_quant_sizes.argtypes = [P(Problem), P(QuantSizes)]
         h.sa2pp_prepass.argtypes = [P(Problem), P(Inputs), P(Quant), C.c_void_p, C.c_size_t, C.c_void_p]
         h.sa2pp_attn_fwd.argtypes = [P(Problem), P(Quant), P(Output), C.c_void_p, C.c_void_p]
+        h.sa2pp_attn_fwd_units.argtypes = [P(Problem), P(Quant), P(Output), C.c_void_p, C.c_int64, C.c_int64,
+                                           C.c_void_p]
         h.sa2pp_sageattn.argtypes = [P(Problem), P(Inputs), P(Quant), C.c_void_p, C.c_size_t,
                                      P(Output), C.c_void_p, C.c_void_p]
         h.sa2pp_set_debug_buffer.argtypes = [C.c_void_p]

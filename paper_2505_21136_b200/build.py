@@ -18,7 +18,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 BUILD = ROOT / "build"
 LIB = PKG / "libsa2pp.so"
-SOURCES = ["sa2pp_api.cu", "prepass.cu", "attn_fwd.cu", "attn_ws.cu", "host_pipeline.cu"]
+SOURCES = ["sa2pp_api.cu", "prepass.cu", "attn_ws.cu", "host_pipeline.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", str(ROOT / "include")]

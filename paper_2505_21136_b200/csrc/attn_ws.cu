@@ -179,12 +179,19 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
-  // ---- work decode: grid = (n_qt, B*Hq); causal runs the heaviest query tiles first
-  const int bh = blockIdx.y;
+  // ---- work decode: grid = (n_qt, heads the unit range touches); CTA (x, y) is unit
+  //      u = (b*Hq + h)*n_qt + qt of head bh = head0 + y, and exits unless u lies in [unit0, unit0 + units)
+  //      (only the partial first/last heads of a q-tile shard have such CTAs); causal runs each head's
+  //      heaviest query tiles first
+  const int bh = p.head0 + static_cast<int>(blockIdx.y);
+  const int qt = CAUSAL ? (p.n_qt - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
+  {
+    const int u = bh * p.n_qt + qt;
+    if (u < p.unit0 || u >= p.unit0 + p.units) return;
+  }
   const int b = bh / p.Hq;
   const int hq = bh % p.Hq;
   const int hkv = hq / p.group;
-  const int qt = CAUSAL ? (p.n_qt - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
   const int q0 = qt * 128;
   const int nblk = CAUSAL ? min(p.n_kb, (min(q0 + 128, p.N) + 63) / 64) : p.n_kb;
 
@@ -231,9 +238,10 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
   const uint32_t tm_row = tmem + (static_cast<uint32_t>(wq * 32) << 16);
   const int row_g = q0 + r;
   const bool row_valid = row_g < p.N;
-  // development trace (INSTR only): clock64 per (block < 64, warp, phase) of the first 8 tiles of head 0
-  unsigned long long* trc = (INSTR && p.trace != nullptr && bh == 0 && qt < 8 && lane == 0)
-                                ? p.trace + static_cast<int64_t>(qt) * 66 * 128 + (warp & 7 | (warp >> 3) << 2) * 16
+  // development trace (INSTR only): clock64 per (block < 64, warp, phase) of every tile of heads 0-2
+  unsigned long long* trc = (INSTR && p.trace != nullptr && bh < 3 && lane == 0)
+                                ? p.trace + static_cast<int64_t>(bh * p.n_qt + qt) * 66 * 128 +
+                                      ((warp & 7) | ((warp >> 3) << 2)) * 16
                                 : nullptr;
   auto stamp = [&](int j, int k) {
     if constexpr (INSTR) {
@@ -596,8 +604,10 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
       const int pb = u % C::kNumPV;
       stamp(j, 0);
       if (!C::kMmaWarp && warp == 4) {  // ---- issue PV(j) [group g], S(j+2), refill of block j-1's stage
-        if (g == 0) mbar_wait_sleep(&p_ready[j & 1], (j >> 1) & 1);
+        if (g == 0) mbar_wait_mode<SA2PP_WS_WAIT_PR>(&p_ready[j & 1], (j >> 1) & 1);
+        stamp(j, 8);
         if (u >= C::kNumPV) mbar_wait(&pv_free[pb], (u / C::kNumPV - 1) & 1);
+        stamp(j, 9);
         tc_fence_after();
         if (elect_one()) {  // one elected region: every UTC* op in a divergent region pays an ELECT loop
           issue_pv(u, j, g);
@@ -612,6 +622,7 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
           if (u >= C::kNumPV && (u - C::kNumPV) % G == G - 1 && jr + S < nblk) load_block(jr + S);
         }
         __syncwarp();
+        stamp(j, 12);
       }
       // ---- promotion of block j (group g): f[c] = dP_j * dV_j[c] for this warp's copy
       mbar_wait_mode<SA2PP_WS_WAIT_PR>(&kv_full[st], (static_cast<unsigned>(j) / S) & 1);  // dV visible
@@ -677,6 +688,33 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
 }
 
 // ------------------------------------------------------------------ host side
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda at link time); the
+// static is written with the same value by any racing first callers.
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+bool make_map_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t rows, uint64_t row_bytes,
+                 uint32_t box_inner, uint32_t box_rows, CUtensorMapSwizzle sw) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {row_bytes};
+  cuuint32_t box[2] = {box_inner, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int D, bool CAUSAL, bool ACC16, bool INSTR, typename OutT, int G>
 static cudaError_t launch_ws_t(const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
   using C = WsCfg<D>;
@@ -695,7 +733,9 @@ static cudaError_t launch_ws_t(const AttnParams& P, const sa2pp_quant& qt, cudaS
     return r;
   });
   if (e != cudaSuccess) return e;
-  dim3 grid(P.n_qt, P.B * P.Hq);
+  if (P.units <= 0) return cudaSuccess;
+  const int h1 = (P.unit0 + P.units - 1) / P.n_qt;
+  dim3 grid(P.n_qt, h1 - P.head0 + 1);
   kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(mq, mk, mv, P);
   return cudaGetLastError();
 }

@@ -240,6 +240,14 @@ int sa2pp_attn_fwd(const sa2pp_problem* p, const sa2pp_quant* qt, const sa2pp_ou
                    void* stream) {
   int rc = sa2pp_check_problem(p);
   if (rc) return rc;
+  const Dims d = dims_of(*p);
+  return sa2pp_attn_fwd_units(p, qt, out, report, 0, static_cast<int64_t>(p->batch) * p->heads_q * d.n_qt, stream);
+}
+
+int sa2pp_attn_fwd_units(const sa2pp_problem* p, const sa2pp_quant* qt, const sa2pp_output* out,
+                         sa2pp_report* report, int64_t unit_begin, int64_t unit_count, void* stream) {
+  int rc = sa2pp_check_problem(p);
+  if (rc) return rc;
   if ((rc = check_quant(qt))) return rc;
   if (!out) return fail(SA2PP_ERR_INVALID, "output is NULL");
   if (out->dtype != SA2PP_F32 && out->dtype != SA2PP_F16 && out->dtype != SA2PP_BF16)
@@ -270,14 +278,15 @@ int sa2pp_attn_fwd(const sa2pp_problem* p, const sa2pp_quant* qt, const sa2pp_ou
   P.report = report;
   P.debug = g_debug;
   P.trace = g_trace;
-  // the v4 kernel chains both k=32 groups in one FP16 accumulator (depth 2 only)
-  const bool depth1_f16 = p->pv_accum == SA2PP_ACC_F16 && p->buffering_depth == 1;
-  static const bool use_v4 = [] {
-    const char* v = std::getenv("SA2PP_ATTN");
-    return v != nullptr && std::strcmp(v, "v4") == 0;
-  }();
-  cudaError_t e = use_v4 && !depth1_f16 ? sa2pp::launch_attn(*p, P, *qt, static_cast<cudaStream_t>(stream))
-                                                : sa2pp::launch_attn_ws(*p, P, *qt, static_cast<cudaStream_t>(stream));
+  const int64_t total = static_cast<int64_t>(p->batch) * p->heads_q * d.n_qt;
+  if (unit_begin < 0 || unit_count < 0 || unit_begin + unit_count > total)
+    return fail(SA2PP_ERR_INVALID, "query-tile units [%lld, %lld) outside [0, %lld)", static_cast<long long>(unit_begin),
+                static_cast<long long>(unit_begin + unit_count), static_cast<long long>(total));
+  if (total > 0x7fffffff) return fail(SA2PP_ERR_UNSUPPORTED, "more than 2^31 - 1 query tiles");
+  P.unit0 = static_cast<int>(unit_begin);
+  P.units = static_cast<int>(unit_count);
+  P.head0 = P.unit0 / P.n_qt;
+  cudaError_t e = sa2pp::launch_attn_ws(*p, P, *qt, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   if (report != nullptr) {  // v_scale min/max over every (key block, channel) (attention.py:271-275)
     e = sa2pp::launch_vscale_minmax(qt->kv_scale64, static_cast<int64_t>(p->batch) * p->heads_kv * d.n_kb, p->head_dim,

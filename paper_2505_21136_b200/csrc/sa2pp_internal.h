@@ -70,10 +70,11 @@ struct AttnParams {
   sa2pp_report* report;
   uint32_t* debug;
   unsigned long long* trace;  // optional per-phase clock trace of a few CTAs (development aid)
+  // query tiles [unit0, unit0 + units) of the flattened (b * Hq + h) * n_qt + qt space (one CTA each)
+  int unit0, units, head0;  // head0 = unit0 / n_qt
 };
 
 cudaError_t launch_prepass(const PrepassLaunch& L, cudaStream_t st);
-cudaError_t launch_attn(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st);
 cudaError_t launch_attn_ws(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st);
 cudaError_t launch_report_init(sa2pp_report* r, cudaStream_t st);
 // min/max of the FP64 V scales [blocks][1 + D] (column 0 is dK) into report->v_scale_{min,max}_bits

@@ -477,3 +477,45 @@ def test_torch_library_op():
     b = sa.sageattn(q, k, v, "HND", True, None)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("causal,hkv", [(False, 6), (True, 3)])
+def test_attn_fwd_units_tile_shards_equal_full_call(causal, hkv):
+    """sa2pp_attn_fwd_units (the q-tile sharding unit, parallel.TilePlan) over every rank's range of a
+    world-5 split reproduces the full sa2pp_attn_fwd bit for bit, and leaves other rows untouched."""
+    import ctypes
+
+    from paper_2505_21136_b200 import _abi as A
+    from paper_2505_21136_b200 import api
+    from paper_2505_21136_b200.parallel import tile_plan
+
+    B, H, N, D = 2, 6, 1000, 128
+    g = torch.Generator(device="cuda").manual_seed(5)
+    q = torch.randn(B, H, N, D, device="cuda", generator=g).bfloat16()
+    k = torch.randn(B, hkv, N, D, device="cuda", generator=g).bfloat16()
+    v = torch.randn(B, hkv, N, D, device="cuda", generator=g).bfloat16()
+    full, qt = sa.sageattn(q, k, v, "HND", causal, None, return_quant=True)
+    prob = api._problem(B, H, hkv, N, D, causal=causal)
+    out = torch.zeros_like(q)
+    o = A.Output(A.SA2PP_BF16, out.data_ptr(), (ctypes.c_int64 * 3)(out.stride(0), out.stride(1), out.stride(2)))
+    qs = qt.struct()
+    lib = A.lib()
+    s = torch.cuda.current_stream().cuda_stream
+    p0 = tile_plan(B, H, hkv, N, 5, 1)
+    A.check(lib.sa2pp_attn_fwd_units(ctypes.byref(prob), ctypes.byref(qs), ctypes.byref(o), None, p0.unit_lo,
+                                     p0.unit_hi - p0.unit_lo, s))
+    torch.cuda.synchronize()
+    flat, ref = out.view(B * H, N, D), full.view(B * H, N, D)
+    done = torch.zeros(B * H, N, dtype=torch.bool, device="cuda")
+    for u in range(p0.unit_lo, p0.unit_hi):
+        h, r0, r1 = p0.unit_rows(u)
+        done[h, r0:r1] = True
+    assert torch.equal(flat[done], ref[done]) and not flat[~done].any()
+    for r in range(5):
+        p = tile_plan(B, H, hkv, N, 5, r)
+        A.check(lib.sa2pp_attn_fwd_units(ctypes.byref(prob), ctypes.byref(qs), ctypes.byref(o), None, p.unit_lo,
+                                         p.unit_hi - p.unit_lo, s))
+    torch.cuda.synchronize()
+    assert torch.equal(out, full)
+    assert lib.sa2pp_attn_fwd_units(ctypes.byref(prob), ctypes.byref(qs), ctypes.byref(o), None, 0,
+                                    p.total_units + 1, s) == A.SA2PP_ERR_INVALID

@@ -77,3 +77,76 @@ def _worker(rank, world, port, causal):
 @pytest.mark.parametrize("causal", [False, True])
 def test_ulysses_gloo_world2_matches_single_process(causal):
     mp.spawn(_worker, args=(2, _free_port(), causal), nprocs=2, join=True)
+
+
+# ----------------------------------------------------------------------------- query-tile sharding
+from paper_2505_21136_b200.parallel import tile_plan  # noqa: E402
+
+
+@pytest.mark.parametrize("B,H,Hkv,N,world", [(2, 30, 30, 17776, 8), (8, 32, 8, 8192, 8), (4, 32, 32, 16384, 3),
+                                              (1, 4, 2, 300, 2), (1, 2, 2, 100, 4)])
+def test_tile_plan_partition(B, H, Hkv, N, world):
+    """Every query tile of every (b, h) belongs to exactly one rank, ranks differ by at most one tile,
+    and each rank's local problem (whole GQA groups) contains its tiles."""
+    seen = []
+    sizes = []
+    for r in range(world):
+        p = tile_plan(B, H, Hkv, N, world, r)
+        lo, hi = p.local_units
+        assert 0 <= lo <= hi <= p.local_heads * p.n_qt
+        assert p.head_lo % p.group == 0 and p.head_hi % p.group == 0
+        assert p.head_lo * p.n_qt <= p.unit_lo and p.unit_hi <= p.head_hi * p.n_qt
+        seen += range(p.unit_lo, p.unit_hi)
+        sizes.append(p.unit_hi - p.unit_lo)
+    assert seen == list(range(B * H * ((N + 127) // 128)))
+    assert max(sizes) - min(sizes) <= 1
+
+
+def _tile_worker(rank, world, port, causal, group):
+    """The bench's sharded path with the oracle standing in for the kernel: each rank takes its
+    TilePlan, quantizes/attends its local heads (HND, batch flattened into heads, as bench.py
+    does) and keeps only its query tiles; the gathered tiles equal the single-process result."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import sage_cpu as oc
+        g = torch.Generator().manual_seed(11)
+        B, H, N, D = 2, 2 * group, 300, 64
+        Hkv = H // group
+        q = torch.randn(B, H, N, D, generator=g, dtype=torch.float64)
+        k = torch.randn(B, Hkv, N, D, generator=g, dtype=torch.float64)
+        v = torch.randn(B, Hkv, N, D, generator=g, dtype=torch.float64)
+        cfg = oc.AttentionConfig(seq_len=N, head_dim=D, causal=causal)
+
+        def head_out(qf, kf, vf, hq):  # flattened HND heads, GQA: kv head hq // group
+            return oc.attention_quantized(qf[hq].numpy(), kf[hq // group].numpy(), vf[hq // group].numpy(), cfg).output
+
+        p = tile_plan(B, H, Hkv, N, world, rank)
+        qf, kf, vf = q.reshape(B * H, N, D), k.reshape(B * Hkv, N, D), v.reshape(B * Hkv, N, D)
+        # local problem: flattened heads [head_lo, head_hi), kv heads [head_lo/group, head_hi/group)
+        ql = qf[p.head_lo:p.head_hi]
+        kl, vl = kf[p.head_lo // group:p.head_hi // group], vf[p.head_lo // group:p.head_hi // group]
+        lo, hi = p.local_units
+        mine = {}
+        for lu in range(lo, hi):
+            hl, t = divmod(lu, p.n_qt)
+            o = head_out(ql, kl, vl, hl)
+            mine[p.head_lo * p.n_qt + lu] = torch.from_numpy(o[t * 128:min(N, t * 128 + 128)])
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine)
+        allu = {}
+        for d in gathered:
+            assert not set(d) & set(allu)
+            allu.update(d)
+        assert sorted(allu) == list(range(p.total_units))
+        for u, o in allu.items():
+            hq, r0, r1 = p.unit_rows(u)
+            ref = head_out(qf, kf, vf, hq)[r0:r1]
+            assert torch.equal(o, torch.from_numpy(ref))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("causal,group", [(False, 1), (True, 2)])
+def test_tile_shard_gloo_world2_matches_single_process(causal, group):
+    mp.spawn(_tile_worker, args=(2, _free_port(), causal, group), nprocs=2, join=True)
