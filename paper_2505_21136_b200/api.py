@@ -7,6 +7,8 @@ the CUDA library.  There is no CPU fallback.
 
 from __future__ import annotations
 
+import warnings
+
 import math
 from dataclasses import dataclass
 from typing import Optional
@@ -308,7 +310,13 @@ def attention_quantized(q, k, v, config: AttentionConfig, *, device: str = "cuda
         raise ValueError(f"tensor shape {arrs[0].shape} does not match config {expected}")
     if not all(np.isfinite(a).all() for a in arrs):
         raise ValueError("Q/K/V must be finite")
-    tq, tk, tv = (torch.from_numpy(a.astype(np.float32))[None].to(device) for a in arrs)
+    a32 = [a.astype(np.float32) for a in arrs]
+    if any(not np.array_equal(x.astype(np.float64), a) for x, a in zip(a32, arrs)):
+        # the kernels read float32/16-bit inputs: quantized tensors are then bit-exact with the
+        # reference run on the float32-rounded inputs, and the output within tolerance of this one
+        warnings.warn("attention_quantized: float64 inputs are not float32-representable and are rounded to "
+                      "float32 for the sm_100a path", RuntimeWarning, stacklevel=2)
+    tq, tk, tv = (torch.from_numpy(a)[None].to(device) for a in a32)
     rep = new_report(tq.device)
     out, qt = sageattn(
         tq, tk, tv, "HND", config.causal, config.scale, pv_accum=config.pv_accumulator,

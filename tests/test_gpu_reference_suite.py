@@ -156,3 +156,33 @@ def test_causal_quantized_matches_reference():  # test_attention.py:275-281
     cos, _, _ = sa.compare(exact(q, k, v, cfg), rep.output)
     assert cos >= 0.999
     assert rep.overflow_events == 0
+
+
+def test_lpattn_tensor_fixture_through_the_gpu():
+    """CPU <-> GPU exchange in the reference's LPATTN-TENSOR v1 files: Q/K/V
+    written by the unmodified reference's `gen` path are loaded straight onto the device with
+    tensorio.load, run through the attention_quantized mirror, and checked against the reference's
+    output file and run row (tests/golden/make_tensor_fixtures.py)."""
+    import json
+    from pathlib import Path
+
+    from paper_2505_21136_b200 import tensorio
+
+    fix = Path(__file__).resolve().parent / "golden" / "lpattn_tensor"
+    row = json.loads((fix / "run.json").read_text())
+    q, k, v = (tensorio.load(fix / f"{n}.bin", device="cuda") for n in ("q", "k", "v"))
+    assert q.is_cuda and q.shape == (row["heads"], row["seq_len"], row["head_dim"])
+    cfg = sa.AttentionConfig(seq_len=row["seq_len"], head_dim=row["head_dim"], num_heads=row["heads"])
+    rep = sa.attention_quantized(q.cpu().numpy(), k.cpu().numpy(), v.cpu().numpy(), cfg)
+    ref_out = tensorio.read_tensor(fix / "out.bin").astype(np.float64)
+    cos, l1, _ = sa.compare(ref_out, rep.output)
+    assert cos >= 0.9999 and l1 <= 1e-3, (cos, l1)
+    assert rep.overflow_events == row["overflow_events"]
+    assert rep.fp16_to_fp32_conversions == row["fp16_to_fp32_conversions"]
+    assert rep.mma_invocations == row["mma_invocations"]
+    ex = exact(q.cpu().double().numpy(), k.cpu().double().numpy(), v.cpu().double().numpy(), cfg)
+    cos_x, l1_x, _ = sa.compare(ex, rep.output)
+    assert cos_x >= row["cossim"] - 1e-4 and l1_x <= row["l1"] + 1e-3, (cos_x, l1_x, row)
+    out_path = Path("/tmp") / "sa2pp_fixture_out.bin"
+    tensorio.save(out_path, torch.from_numpy(rep.output))  # and back into the reference's format
+    assert np.allclose(tensorio.read_tensor(out_path), rep.output.astype(np.float32))

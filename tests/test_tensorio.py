@@ -40,3 +40,22 @@ def test_interchangeable_with_reference(lpattn, tmp_path):
     tio.write_tensor(tmp_path / "o.bin", x)
     assert (tmp_path / "r.bin").read_bytes() == (tmp_path / "o.bin").read_bytes()
     assert np.array_equal(ref.read_tensor(tmp_path / "o.bin"), tio.read_tensor(tmp_path / "r.bin"))
+
+
+FIX = __import__("pathlib").Path(__file__).resolve().parent / "golden" / "lpattn_tensor"
+
+
+def test_reference_tensor_fixture_oracle_parity():
+    """The LPATTN-TENSOR fixture written by the unmodified reference (tests/golden/make_tensor_fixtures.py)
+    reads back through this reader and the oracle reproduces the reference's output file and run row."""
+    import json
+
+    from oracle import sage_cpu as oc
+    q, k, v = (tio.read_tensor(FIX / f"{n}.bin") for n in ("q", "k", "v"))
+    ref_out = tio.read_tensor(FIX / "out.bin")
+    row = json.loads((FIX / "run.json").read_text())
+    cfg = oc.AttentionConfig(seq_len=row["seq_len"], head_dim=row["head_dim"], num_heads=row["heads"])
+    rep = oc.attention_quantized(q, k, v, cfg)
+    assert np.array_equal(rep.output.astype(np.float32), ref_out)
+    assert rep.overflow_events == row["overflow_events"]
+    assert json.loads((FIX / "q.bin.meta.json").read_text())["distribution"] == "gaussian"

@@ -72,6 +72,10 @@ __global__ void bench(int iters, uint32_t* sink, unsigned long long* cyc) {
         asm volatile("{.reg .f16 l, h;\n mov.b32 {l, h}, %2;\n add.rn.f32.f16 %0, l, %3;\n add.rn.f32.f16 %1, h, %3;}"
                      : "=f"(a), "=f"(b) : "r"(r[i]), "f"(-0.0f));
         r[i] = __float_as_uint(a) ^ __float_as_uint(b);
+      } else if constexpr (OP == 12) {  // MUFU.EX2 on f16x2: two exponentials per lane
+        asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(r[i]));
+      } else if constexpr (OP == 13) {  // MUFU.EX2 on bf16x2
+        asm volatile("ex2.approx.ftz.bf16x2 %0, %0;" : "+r"(r[i]));
       } else if constexpr (OP == 10) {  // PRMT
         asm volatile("prmt.b32 %0, %0, %1, 0x5410;" : "+r"(r[i]) : "r"(r[(i + 3) & 7]));
       }
@@ -118,5 +122,7 @@ int main() {
   run<9>("FADD2 (add.rn.f32x2)", 1, sms, sink, cyc);
   run<10>("PRMT", 1, sms, sink, cyc);
   run<11>("FHADD (add.rn.f32.f16), per conversion", 2, sms, sink, cyc);
+  run<12>("MUFU.EX2 f16x2 (2 exps per lane)", 1, sms, sink, cyc);
+  run<13>("MUFU.EX2 bf16x2 (2 exps per lane)", 1, sms, sink, cyc);
   return 0;
 }

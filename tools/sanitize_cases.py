@@ -26,6 +26,7 @@ CASES = [
     (1, 2, 2, 777, 64, True, "fp16"),
     (1, 1, 1, 1100, 128, False, "fp32"),
     (1, 1, 1, 17776 // 8, 64, False, "fp16"),  # the CogVideoX ragged tail (48 real keys in the last block)
+    (1, 2, 2, 640, 128, False, "fp16-depth1"),  # buffering depth 1: each k=32 group its own FP16 accumulation
 ]
 
 
@@ -38,9 +39,10 @@ def main() -> None:
         q = torch.randn(B, Hq, N, D, device="cuda", dtype=torch.bfloat16, generator=g)
         k = torch.randn(B, Hkv, N, D, device="cuda", dtype=torch.bfloat16, generator=g)
         v = torch.randn(B, Hkv, N, D, device="cuda", dtype=torch.bfloat16, generator=g)
-        o = sa.sageattn(q, k, v, "HND", causal, None, pv_accum=acc)
+        kw = dict(pv_accum="fp16", buffering_depth=1) if acc == "fp16-depth1" else dict(pv_accum=acc)
+        o = sa.sageattn(q, k, v, "HND", causal, None, **kw)
         rep = sa.new_report("cuda")
-        o2 = sa.sageattn(q, k, v, "HND", causal, None, pv_accum=acc, report=rep)
+        o2 = sa.sageattn(q, k, v, "HND", causal, None, report=rep, **kw)
         torch.cuda.synchronize()
         ok = torch.equal(o, o2)
         print(f"case {i}: B={B} Hq={Hq} Hkv={Hkv} N={N} D={D} causal={causal} acc={acc} "
