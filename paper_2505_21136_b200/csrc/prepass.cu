@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(256, 2) quantize_q_kernel(InView qv, int Hq, i
     }
     const double inv = 1.0 / scale;
     const float inv32 = static_cast<float>(inv);
-    const bool fast = mumax <= 65536.0 * amax && amax >= 0x1p-100;  // see quantize_kv
+    const bool fast = mumax <= 65536.0 * amax && amax >= 0x1p-100;  // see quantize_k
 
     // codes: ((q - mu_hi) - mu_lo) * inv rounded with the 1.5*2^23 trick; the code is the low byte
     // of the rounded float's bits (|q| <= qmax + 3e-5 under `fast`, so no clamp is needed)
