@@ -59,11 +59,16 @@ __device__ __forceinline__ const T* row_ptr(const InView& v, int b, int h, int n
 // numpy's x.mean(axis=0) over a C-ordered (N, D) float64 array is a SEQUENTIAL float64 sum per
 // channel in token order followed by one division by N (quantization.py:133,147; checked against
 // numpy in tests/test_gpu_parity.py), so each channel is one FP64 add chain here too: one CTA per
-// (b, head) of Q and K, thread t owns channels {2t, 2t+1}; the head's rows stream through a 4-stage
-// cp.async ring in shared memory (16 KB per stage) and every thread adds its two channels row by row.
+// (b, head) of Q and K, thread t owns channel t (SA2PP_MEANS_CPT = 1; 2 was 5 % slower); the head's rows
+// stream through a 4-stage cp.async ring in shared memory (16 KB per stage) and every thread adds its
+// channel row by row.  The FP64 add chain (one dependent add per token) sets the kernel's time.
+#ifndef SA2PP_MEANS_CPT
+#define SA2PP_MEANS_CPT 1  // channels (independent FP64 add chains) per thread
+#endif
 template <typename T, int D>
 struct MeansCfg {
-  static constexpr int kThreads = D / 2;
+  static constexpr int kCpt = SA2PP_MEANS_CPT;
+  static constexpr int kThreads = D / kCpt;
   static constexpr int kRowBytes = D * static_cast<int>(sizeof(T));
   static constexpr int kStageBytes = 16384;
   static constexpr int kRows = kStageBytes / kRowBytes;  // rows per stage
@@ -89,7 +94,7 @@ __device__ __forceinline__ void two_f64(const void* p, double& a, double& b) {
 }
 
 template <typename T, int D>
-__global__ void __launch_bounds__(D / 2) channel_means_kernel(InView qv, InView kv, int Hq, int Hkv, int N,
+__global__ void __launch_bounds__(D / SA2PP_MEANS_CPT) channel_means_kernel(InView qv, InView kv, int Hq, int Hkv, int N,
                                                               double* __restrict__ means) {
   using M = MeansCfg<T, D>;
   extern __shared__ __align__(16) unsigned char ms_smem[];
@@ -122,9 +127,12 @@ __global__ void __launch_bounds__(D / 2) channel_means_kernel(InView qv, InView 
     asm volatile("cp.async.wait_group %0;" ::"n"(M::kStages - 2) : "memory");
     __syncthreads();  // stage s landed for every thread; stage s-1 is no longer read
     issue(s + M::kStages - 1);
-    const unsigned char* src = ms_smem + (s % M::kStages) * M::kStageBytes + t * 2 * sizeof(T);
+    const unsigned char* src = ms_smem + (s % M::kStages) * M::kStageBytes + t * M::kCpt * sizeof(T);
     const int rows = min(M::kRows, N - s * M::kRows);
-    if (rows == M::kRows) {
+    if constexpr (M::kCpt == 1) {
+#pragma unroll 16
+      for (int r = 0; r < rows; ++r) s0 += static_cast<double>(to_f32<T>(*reinterpret_cast<const T*>(src + r * M::kRowBytes)));
+    } else if (rows == M::kRows) {
 #pragma unroll 16
       for (int r = 0; r < M::kRows; ++r) {
         double a, c;
@@ -143,6 +151,10 @@ __global__ void __launch_bounds__(D / 2) channel_means_kernel(InView qv, InView 
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
   const double n = static_cast<double>(N);
+  if constexpr (M::kCpt == 1) {
+    means[static_cast<int64_t>(bh) * D + t] = s0 / n;
+    return;
+  }
   *reinterpret_cast<double2*>(means + static_cast<int64_t>(bh) * D + 2 * t) = make_double2(s0 / n, s1 / n);
 }
 
@@ -497,8 +509,11 @@ __device__ __forceinline__ void load_rows(const InView& in, int b, int h, int n0
   }
 }
 
+#ifndef SA2PP_K_MINB
+#define SA2PP_K_MINB 3
+#endif
 template <typename T, int D>
-__global__ void __launch_bounds__(256, 3) quantize_k_kernel(InView kv_in, int Hq, int Hkv, int N, int Np, int n_kb,
+__global__ void __launch_bounds__(256, SA2PP_K_MINB) quantize_k_kernel(InView kv_in, int Hq, int Hkv, int N, int Np, int n_kb,
                                                             int qmax, int smoothing, double sm_scale_log2,
                                                             const double* __restrict__ means, int Ht,
                                                             int8_t* __restrict__ k_codes, float* __restrict__ kv_meta,
@@ -706,8 +721,11 @@ __host__ __device__ constexpr int v_smem_bytes() {
   return 8 * D * 4 + D * 64 + D * 8 + D * 4;
 }
 
+#ifndef SA2PP_V_MINB
+#define SA2PP_V_MINB 4
+#endif
 template <typename T, int D>
-__global__ void __launch_bounds__(256, 3) quantize_v_kernel(InView v_in, int Hkv, int N, int Np, int n_kb, double v_r,
+__global__ void __launch_bounds__(256, SA2PP_V_MINB) quantize_v_kernel(InView v_in, int Hkv, int N, int Np, int n_kb, double v_r,
                                                             uint8_t* __restrict__ v_codes, float* __restrict__ kv_meta,
                                                             double* __restrict__ kv_scale64) {
   using G = KvGeom<T, D>;
