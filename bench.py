@@ -240,14 +240,29 @@ def run_ours(a):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SA2PP_BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0 with gloo collectives on host tensors,
+    # so the multi-rank sharding path runs on a one-GPU box; numbers from it are not bench values
+    share = os.environ.get("SA2PP_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def max_over_ranks(vals):
+        if world == 1:
+            return list(vals)
+        t = torch.tensor(list(vals), dtype=torch.float64, device="cpu" if share else dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
 
     B, H, Hkv, N, D = a.batch, a.heads, a.kv_heads, a.seq, a.head_dim
     group = H // Hkv
-    ulysses = a.workload == "longctx" and world > 1
+    ulysses = a.workload == "longctx" and world > 1 and not share
     if ulysses:
         # sequence-sharded input [1, N/P, H, D] per rank; all-to-all to [1, N, H/P, D] and back
         Ul, Nl = H // world, N // world
@@ -343,10 +358,7 @@ def run_ours(a):
         total_ms = sum(e0.elapsed_time(e2) for e0, _, e2 in ev)
     attn_ms = statistics.mean(e1.elapsed_time(e2) for _, e1, e2 in ev)
     pre_ms = statistics.mean(e0.elapsed_time(e1) for e0, e1, _ in ev)
-    if world > 1:
-        t = torch.tensor([total_ms, attn_ms, pre_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, attn_ms, pre_ms = t.tolist()
+    total_ms, attn_ms, pre_ms = max_over_ranks([total_ms, attn_ms, pre_ms])
     ms_per_step = total_ms / a.steps
     job_ops = ops_of(B, H, N, D, a.causal)  # all ranks together
     value = job_ops / (ms_per_step * 1e-3) / 1e12
@@ -381,10 +393,7 @@ def run_ours(a):
         s1.record(stream)
         torch.cuda.synchronize(dev)
         e2e_ms = s0.elapsed_time(s1) / n_e2e
-        if world > 1:
-            t = torch.tensor([e2e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e2e_ms = t.item()
+        e2e_ms = max_over_ranks([e2e_ms])[0]
         e2e = {"value": job_ops / (e2e_ms * 1e-3) / 1e12, "unit": "TOPS",
                "h2d_bytes_per_step": sum(t.numel() * t.element_size() for t in (hq, hk, hv)) * world,
                "d2h_bytes_per_step": ho.numel() * ho.element_size() * world,

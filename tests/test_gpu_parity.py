@@ -519,3 +519,31 @@ def test_attn_fwd_units_tile_shards_equal_full_call(causal, hkv):
     assert torch.equal(out, full)
     assert lib.sa2pp_attn_fwd_units(ctypes.byref(prob), ctypes.byref(qs), ctypes.byref(o), None, 0,
                                     p.total_units + 1, s) == A.SA2PP_ERR_INVALID
+
+
+def test_bench_sharded_path_two_ranks_on_one_gpu():
+    """bench.py's multi-rank q-tile sharding path end to end (torchrun, world 2): with
+    SA2PP_BENCH_SHARE_GPU=1 both ranks run their TilePlan units on cuda:0 and reduce timings over
+    gloo; rank 0 prints one JSON line (the driver's 8-GPU run uses NCCL and one GPU per rank)."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    with socket.socket() as s_:
+        s_.bind(("127.0.0.1", 0))
+        port = s_.getsockname()[1]
+    env = dict(os.environ, SA2PP_BENCH_SHARE_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(root / "bench.py"),
+           "--gpus", "2", "--workload", "cogvideox", "--seq", "2000", "--steps", "2", "--warmup", "3",
+           "--no-e2e", "--no-cpu"]
+    r = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "q-tile shard x2" and d["value"] > 0
