@@ -848,12 +848,73 @@ __global__ void __launch_bounds__(256, SA2PP_V_MINB) quantize_v_kernel(InView v_
 }
 
 // ------------------------------------------------------------------ host launcher
+// A non-blocking side stream and its fork/join events, per calling thread and device (created on
+// first use, destroyed with the thread); nullptr stream = run everything on the caller's stream.
+struct SideStream {
+  cudaStream_t stream = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  int dev = -1;
+  ~SideStream() {
+    if (stream != nullptr) {
+      int cur = 0;
+      if (cudaGetDevice(&cur) == cudaSuccess && cur != dev) cudaSetDevice(dev);
+      cudaEventDestroy(fork);
+      cudaEventDestroy(join);
+      cudaStreamDestroy(stream);
+      if (cur != dev) cudaSetDevice(cur);
+    }
+  }
+};
+
+static SideStream& side_stream() {
+  static thread_local SideStream per_dev[16];
+  static SideStream none;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return none;
+  SideStream& s = per_dev[dev];
+  if (s.stream == nullptr) {
+    if (cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking) != cudaSuccess) {
+      s.stream = nullptr;
+      return none;
+    }
+    if (cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaStreamDestroy(s.stream);
+      s.stream = nullptr;
+      return none;
+    }
+    s.dev = dev;
+  }
+  return s;
+}
+
 template <typename T, int D>
 static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
   InView qv{L.q, L.q_stride[0], L.q_stride[1], L.q_stride[2]};
   InView kv{L.k, L.k_stride[0], L.k_stride[1], L.k_stride[2]};
   InView vv{L.v, L.v_stride[0], L.v_stride[1], L.v_stride[2]};
   const int Ht = L.Hq + L.Hkv;
+  // quantize_v needs no channel means, so it runs on a side stream beside channel_means (a long FP64
+  // add chain on few CTAs) and quantize_q/k; the caller's stream joins it at the end (fork/join is
+  // stream-ordered and graph-capturable).  quantize_q beside quantize_k was measured too: no gain at
+  // 16K (both near their own limits)
+  const dim3 gk(L.n_kb, L.B * L.Hkv);
+  constexpr int v_smem = v_smem_bytes<T, D>();
+  {
+    static PerDevice v_once;
+    cudaError_t e = v_once.run([&](std::atomic<int>&) {
+      return cudaFuncSetAttribute(quantize_v_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, v_smem);
+    });
+    if (e != cudaSuccess) return e;
+  }
+  SideStream& side = side_stream();
+  if (side.stream != nullptr) {
+    cudaError_t e = cudaEventRecord(side.fork, st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(side.stream, side.fork, 0);
+    if (e != cudaSuccess) return e;
+    quantize_v_kernel<T, D><<<gk, 256, v_smem, side.stream>>>(vv, L.Hkv, L.N, L.Np, L.n_kb, L.v_r, L.v_codes,
+                                                              L.kv_meta, L.kv_scale64);
+  }
   if (L.smoothing) {
     using M = MeansCfg<T, D>;
     constexpr int smem = M::kStages * M::kStageBytes;
@@ -886,17 +947,16 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
     quantize_q_kernel<T, D><<<grid, 256, q_smem, st>>>(qv, L.Hq, L.N, L.Nq_pad, L.n_qt, n_tiles, L.qmax, L.means, Ht,
                                                        L.q_codes, L.q_scale, L.q_scale64);
   }
-  dim3 gk(L.n_kb, L.B * L.Hkv);
   quantize_k_kernel<T, D><<<gk, 256, 0, st>>>(kv, L.Hq, L.Hkv, L.N, L.Np, L.n_kb, L.qmax, L.smoothing, L.sm_scale_log2,
                                               L.means, Ht, L.k_codes, L.kv_meta, L.kv_scale64, L.bias, L.bias_l2);
-  constexpr int v_smem = v_smem_bytes<T, D>();
-  static PerDevice v_once;
-  cudaError_t e = v_once.run([&](std::atomic<int>&) {
-    return cudaFuncSetAttribute(quantize_v_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, v_smem);
-  });
-  if (e != cudaSuccess) return e;
-  quantize_v_kernel<T, D><<<gk, 256, v_smem, st>>>(vv, L.Hkv, L.N, L.Np, L.n_kb, L.v_r, L.v_codes, L.kv_meta,
-                                                   L.kv_scale64);
+  if (side.stream != nullptr) {  // join: the caller's stream waits for quantize_v
+    cudaError_t e = cudaEventRecord(side.join, side.stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(st, side.join, 0);
+    if (e != cudaSuccess) return e;
+  } else {
+    quantize_v_kernel<T, D><<<gk, 256, v_smem, st>>>(vv, L.Hkv, L.N, L.Np, L.n_kb, L.v_r, L.v_codes, L.kv_meta,
+                                                     L.kv_scale64);
+  }
   return cudaGetLastError();
 }
 
