@@ -46,4 +46,21 @@ def zeros_subnormals():
     return q, k, v, True
 
 
-CASES = {"exact_ties": exact_ties, "huge_offsets": huge_offsets, "zeros_subnormals": zeros_subnormals}
+def tiny_blocks():
+    """Whole blocks / block channels whose amax is below 2^-100 (subnormals mixed with zeros): the f32
+    reciprocal of the scale would overflow, so the exact FP64 path must run."""
+    rng = np.random.default_rng(14)
+    n, d = 256, 64
+    q = rng.normal(size=(2, n, d)).astype(np.float32)
+    k = rng.normal(size=(2, n, d)).astype(np.float32)
+    v = rng.normal(size=(2, n, d)).astype(np.float32)
+    v[0, 64:128, 5] = (np.float32(1e-40) * rng.integers(0, 3, size=64)).astype(np.float32)  # subnormal + zeros
+    v[1, 128:192, 9] = np.float32(3e-38) * rng.choice([-1.0, 0.0, 0.5, 1.0], size=64).astype(np.float32)
+    v[1, 192:256, :] = np.float32(2e-39) * rng.integers(-2, 3, size=(64, d)).astype(np.float32)  # a whole block
+    k[1, 0:64, :] = (np.float32(1e-39) * rng.integers(-3, 4, size=(64, d))).astype(np.float32)  # K block amax tiny
+    q[0, 0:128, :] = (np.float32(5e-39) * rng.normal(size=(128, d))).astype(np.float32)  # Q tile amax tiny
+    return q, k, v, False
+
+
+CASES = {"exact_ties": exact_ties, "huge_offsets": huge_offsets, "zeros_subnormals": zeros_subnormals,
+         "tiny_blocks": tiny_blocks}

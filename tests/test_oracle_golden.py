@@ -155,7 +155,7 @@ def test_live_reference_on_fresh_seed(lpattn):
     assert ours.mma_invocations == ref.mma_invocations
 
 
-@pytest.mark.parametrize("case", ["exact_ties", "huge_offsets", "zeros_subnormals"])
+@pytest.mark.parametrize("case", ["exact_ties", "huge_offsets", "zeros_subnormals", "tiny_blocks"])
 def test_oracle_prepass_edges_vs_live_reference(lpattn, case):
     """The oracle's quantizers equal the reference's on the adversarial inputs the GPU prepass is
     tested with (tests/test_gpu_prepass_edges.py): ties, huge offsets, zeros, subnormals."""
