@@ -178,8 +178,17 @@ class ClockSampler:
             self.proc = None
         return self
 
+    def wait_started(self, timeout: float = 3.0):
+        """Block until the sampler has written its first row (so the timed region is covered)."""
+        t0 = time.time()
+        while self.proc is not None and time.time() - t0 < timeout:
+            if self.path.exists() and self.path.stat().st_size > 0:
+                return
+            time.sleep(0.05)
+
     def __exit__(self, *exc):
         if self.proc is not None:
+            time.sleep(0.25)  # one more sample after the last timed step
             self.proc.terminate()
             self.proc.wait(timeout=5)
 
@@ -322,6 +331,10 @@ def run_ours(a):
     resident = sum(t.numel() * t.element_size() for t in (q, k, v, out))
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if resident < 2 * (126 << 20) else None
 
+    # the clock sampler starts before the warm-up (nvidia-smi needs ~0.3 s to report) and keeps going
+    # until the timed steps are done; it must not be the thing that is slow to start
+    clk = ClockSampler(local).__enter__()
+    clk.wait_started()
     for _ in range(a.warmup):
         exchange_in()
         prepass()
@@ -332,7 +345,7 @@ def run_ours(a):
         dist.barrier()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
            torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
-    with ClockSampler(local) as clk:
+    with clk:
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
