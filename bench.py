@@ -166,6 +166,8 @@ class ClockSampler:
         self.path = Path(f"/tmp/sa2pp_clocks_{os.getpid()}.csv")
 
     def __enter__(self):
+        if self.proc is not None:  # already sampling (started before the warm-up)
+            return self
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.idx}",
@@ -174,9 +176,19 @@ class ClockSampler:
                  "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
                  "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            import atexit
+            atexit.register(self.stop)  # never leave a sampler behind, whatever happens in between
         except Exception:
             self.proc = None
         return self
+
+    def stop(self):
+        if self.proc is not None and self.proc.poll() is None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
 
     def wait_started(self, timeout: float = 3.0):
         """Block until the sampler has written its first row (so the timed region is covered)."""
@@ -189,8 +201,7 @@ class ClockSampler:
     def __exit__(self, *exc):
         if self.proc is not None:
             time.sleep(0.25)  # one more sample after the last timed step
-            self.proc.terminate()
-            self.proc.wait(timeout=5)
+            self.stop()
 
     def summary(self):
         if self.proc is None or not self.path.exists():
