@@ -547,3 +547,56 @@ def test_bench_sharded_path_two_ranks_on_one_gpu():
     assert len(lines) == 1, r.stdout
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "q-tile shard x2" and d["value"] > 0
+
+
+def test_cuda_graph_capture_and_replay():
+    """The whole sageattn (prepass incl. its side-stream fork/join + attention) captures into a CUDA graph
+    (the device entry points never allocate or synchronise); replays on new inputs equal eager calls."""
+    B, H, N, D = 2, 4, 700, 128
+    g = torch.Generator(device="cuda").manual_seed(9)
+    q, k, v = (torch.randn(B, H, N, D, device="cuda", generator=g).bfloat16() for _ in range(3))
+    out = torch.empty_like(q)
+    quant = sa.quantize(q, k, v)  # buffers reused by the captured call
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        sa.sageattn(q, k, v, out=out, quant=quant)  # warm-up (function attributes, side stream)
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        sa.sageattn(q, k, v, out=out, quant=quant)
+    for seed in (1, 2):
+        g2 = torch.Generator(device="cuda").manual_seed(seed)
+        for t in (q, k, v):
+            t.copy_(torch.randn(t.shape, device="cuda", generator=g2).bfloat16())
+        graph.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, sa.sageattn(q, k, v))
+
+
+def test_concurrent_calls_from_two_threads():
+    """Two host threads issuing sageattn on their own streams at once (each thread has its own prepass
+    side stream) give the same bits as serial calls."""
+    import threading
+
+    g = torch.Generator(device="cuda").manual_seed(10)
+    cases = [tuple(torch.randn(1, 8, 2000, 64, device="cuda", generator=g).bfloat16() for _ in range(3))
+             for _ in range(2)]
+    ref = [sa.sageattn(*c) for c in cases]
+    torch.cuda.synchronize()
+    res = [None, None]
+
+    def run(i):
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            for _ in range(5):
+                res[i] = sa.sageattn(*cases[i])
+        st.synchronize()
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    torch.cuda.synchronize()
+    assert all(torch.equal(a, b) for a, b in zip(res, ref))
