@@ -53,23 +53,7 @@
 #ifndef SA2PP_WS_STAGES128
 #define SA2PP_WS_STAGES128 4
 #endif
-// 1: a ninth warp issues every tcgen05.mma and TMA copy, so the promotion warps only promote (the
-// issue latency -- each UMMA blocks its issuing thread until the tensor pipe takes it -- otherwise sits
-// on the promotion chain that gates the next PV and S).  Registers (2 CTAs x 288 threads, 112 each at
-// launch): softmax SA2PP_WS_REG_SM_M, promotion SA2PP_WS_REG_PR_M, MMA warp SA2PP_WS_REG_MMA.
-#ifndef SA2PP_WS_MMA_WARP
-#define SA2PP_WS_MMA_WARP 0
-#endif
-#ifndef SA2PP_WS_REG_SM_M
-#define SA2PP_WS_REG_SM_M 80
-#endif
-#ifndef SA2PP_WS_REG_PR_M
-#define SA2PP_WS_REG_PR_M 160
-#endif
-#ifndef SA2PP_WS_REG_MMA
-#define SA2PP_WS_REG_MMA 48
-#endif
-// mbarrier wait policy (ptx.cuh mbar_wait_mode) of the softmax, promotion and MMA warps
+// mbarrier wait policy (ptx.cuh mbar_wait_mode) of the softmax and promotion warps
 // timing probes (wrong results): half of the promotion's channels / half of the exponentials
 #ifndef SA2PP_WS_PROBE_HALFPROMO
 #define SA2PP_WS_PROBE_HALFPROMO 0
@@ -88,9 +72,6 @@
 #endif
 #ifndef SA2PP_WS_WAIT_PR
 #define SA2PP_WS_WAIT_PR 0
-#endif
-#ifndef SA2PP_WS_WAIT_MMA
-#define SA2PP_WS_WAIT_MMA 0
 #endif
 
 namespace sa2pp {
@@ -127,21 +108,17 @@ struct WsCfg {
   static constexpr int kNumBars = 1 + kStages + 2 + 2 + 2 * kNumPV + 2 + 1;
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmemBytes = kOffTmem + 16 + 1024;  // + alignment slack
-  // D=128 cannot afford the ninth warp: the register file is split per SMSP (16384 each), so with
-  // 2 x 9 warps one SMSP holds 6 warps and the launch allocation drops to 96 per thread (27648 per
-  // CTA), below the 128 x (88 + 168) the two warpgroups need.
-  static constexpr bool kMmaWarp = SA2PP_WS_MMA_WARP != 0 && D == 64;
-  static constexpr int kThreads = kMmaWarp ? 288 : 256;
-  static constexpr uint32_t kRegLaunch = kMmaWarp ? 96 : 128;  // 16384 / (32 x max warps per SMSP), x8
+  // No ninth (MMA-issue) warp: the register file is split per SMSP (16384 each), so with 2 x 9 warps
+  // one SMSP holds 6 warps and the launch allocation drops to 96 per thread (27648 per CTA), below the
+  // 128 x (88 + 168) the two warpgroups need at D=128 (a D=64 variant measured neutral).
+  static constexpr int kThreads = 256;
+  static constexpr uint32_t kRegLaunch = 128;  // 65536 / (2 CTAs x 256 threads)
   // register split (setmaxnreg) at D=128; D=64 keeps the launch allocation everywhere
-  static constexpr uint32_t kRegSoftmax =
-      (D == 128) ? (kMmaWarp ? SA2PP_WS_REG_SM_M : SA2PP_WS_REG_SOFTMAX) : kRegLaunch;
-  static constexpr uint32_t kRegPromote =
-      (D == 128) ? (kMmaWarp ? SA2PP_WS_REG_PR_M : 256 - SA2PP_WS_REG_SOFTMAX) : kRegLaunch;
-  static constexpr uint32_t kRegMma = (D == 128) ? SA2PP_WS_REG_MMA : kRegLaunch;
+  static constexpr uint32_t kRegSoftmax = (D == 128) ? SA2PP_WS_REG_SOFTMAX : kRegLaunch;
+  static constexpr uint32_t kRegPromote = (D == 128) ? 256 - SA2PP_WS_REG_SOFTMAX : kRegLaunch;
   static constexpr int kPvChunk16 = SA2PP_WS_PV_CHUNK;  // FP16-accumulator channels per TMEM load
   static constexpr int kLdPipe = SA2PP_WS_LDPIPE >= 0 ? SA2PP_WS_LDPIPE : (D == 64 ? 1 : 0);
-  static_assert(128 * (kRegSoftmax + kRegPromote) + (kMmaWarp ? 32 * kRegMma : 0) <= kThreads * kRegLaunch,
+  static_assert(128 * (kRegSoftmax + kRegPromote) <= kThreads * kRegLaunch,
                 "the warpgroups share the launch register budget");
   static_assert(2 * kSmemBytes <= 227 * 1024, "two CTAs per SM must fit in shared memory");
 };
@@ -248,7 +225,7 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
   // development trace (INSTR only): clock64 per (block < 64, warp, phase) of every tile of heads 0-2
   unsigned long long* trc = (INSTR && p.trace != nullptr && bh < 3 && lane == 0)
                                 ? p.trace + static_cast<int64_t>(bh * p.n_qt + qt) * 66 * 128 +
-                                      ((warp & 7) | ((warp >> 3) << 2)) * 16
+                                      warp * 16
                                 : nullptr;
   auto stamp = [&](int j, int k) {
     if constexpr (INSTR) {
@@ -445,13 +422,8 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
     __syncwarp();
     if (lane == 0) mbar_arrive(l_ready);
   } else {
-    // ====================== promotion warpgroup (+ issue), or the MMA warp ======================
-    const bool mma_warp = C::kMmaWarp && warp == 8;
-    if (mma_warp) {
-      if constexpr (C::kRegMma < C::kRegLaunch) setmaxnreg_dec<C::kRegMma>();
-    } else {
-      if constexpr (C::kRegPromote > C::kRegLaunch) setmaxnreg_inc<C::kRegPromote>();
-    }
+    // =============================== promotion warpgroup (+ issue) ===============================
+    if constexpr (C::kRegPromote > C::kRegLaunch) setmaxnreg_inc<C::kRegPromote>();
     const int kv_row = (b * p.Hkv + hkv) * p.Np;
     const int vt_row = (b * p.Hkv + hkv) * D;
     const float* meta_src = p.kv_meta + static_cast<int64_t>(b * p.Hkv + hkv) * p.n_kb * (4 + D);
@@ -490,7 +462,7 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
       }
       umma_commit(&pv_full[pb]);
     };
-    if (warp == (C::kMmaWarp ? 8 : 4) && elect_one()) {
+    if (warp == 4 && elect_one()) {
       tma_prefetch_desc(&tm_q);
       tma_prefetch_desc(&tm_k);
       tma_prefetch_desc(&tm_v);
@@ -507,34 +479,6 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
     }
     __syncwarp();
 
-    if (mma_warp) {
-      // ---- MMA warp: PV(j) [group g] once P^(j) is stored and the PV buffer drained, S(j+2) right
-      //      behind it (in-order tcgen05 execution: PV(j) has read P^(j) before S(j+2) overwrites
-      //      those columns), and the TMA refill of the stage whose readers are all done.
-      if (elect_one()) {
-        for (int u = 0; u < nblk * G; ++u) {
-          const int j = (G == 1) ? u : (u >> 1);
-          const int g = (G == 1) ? 0 : (u & 1);
-          const int pb = u % C::kNumPV;
-          if (g == 0) mbar_wait_mode<SA2PP_WS_WAIT_MMA>(&p_ready[j & 1], (j >> 1) & 1);
-          stamp(j, 8);
-          if (u >= C::kNumPV) mbar_wait_mode<SA2PP_WS_WAIT_MMA>(&pv_free[pb], (u / C::kNumPV - 1) & 1);
-          stamp(j, 9);
-          tc_fence_after();
-          issue_pv(u, j, g);
-          if (g == G - 1 && j + 2 < nblk) {
-            mbar_wait_mode<SA2PP_WS_WAIT_MMA>(&kv_full[static_cast<unsigned>(j + 2) % S],
-                                              (static_cast<unsigned>(j + 2) / S) & 1);
-            issue_qk(j + 2);
-          }
-          stamp(j, 10);
-          const int jr = (u - C::kNumPV) / G;  // block whose promotion is complete
-          if (u >= C::kNumPV && (u - C::kNumPV) % G == G - 1 && jr + S < nblk) load_block(jr + S);
-          stamp(j, 12);
-        }
-      }
-      __syncwarp();
-    } else {
     const int pw = warp - 4;  // promotion warp index = TMEM lane quarter
     float* fw = reinterpret_cast<float*>(smem + C::kOffF) + pw * D;
     const bool dbg = INSTR && (p.debug != nullptr) && qt == 0 && bh == 0;
@@ -649,7 +593,7 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
       const int st = static_cast<int>(static_cast<unsigned>(j) % S);
       const int pb = u % C::kNumPV;
       stamp(j, 0);
-      if (!C::kMmaWarp && warp == 4) {  // ---- issue PV(j) [group g], S(j+2), refill of block j-1's stage
+      if (warp == 4) {  // ---- issue PV(j) [group g], S(j+2), refill of block j-1's stage
         if (g == 0) mbar_wait_mode<SA2PP_WS_WAIT_PR>(&p_ready[j & 1], (j >> 1) & 1);
         stamp(j, 8);
         if (u >= C::kNumPV) mbar_wait(&pv_free[pb], (u / C::kNumPV - 1) & 1);
@@ -719,7 +663,6 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
       OutT* dst = reinterpret_cast<OutT*>(p.out) + b * p.o_sb + hq * p.o_sh + static_cast<int64_t>(row_g) * p.o_sn;
       store_row<D, OutT>(dst, O, inv_l);
     }
-    }  // promotion warps
   }
 
   tc_fence_before();
