@@ -53,6 +53,9 @@
 #ifndef SA2PP_WS_STAGES128
 #define SA2PP_WS_STAGES128 4
 #endif
+#ifndef SA2PP_WS_STAGES64
+#define SA2PP_WS_STAGES64 8
+#endif
 // mbarrier wait policy (ptx.cuh mbar_wait_mode) of the softmax and promotion warps
 // timing probes (wrong results): half of the promotion's channels / half of the exponentials
 #ifndef SA2PP_WS_PROBE_HALFPROMO
@@ -78,7 +81,7 @@ namespace sa2pp {
 
 template <int D>
 struct WsCfg {
-  static constexpr int kStages = (D == 128) ? SA2PP_WS_STAGES128 : 8;
+  static constexpr int kStages = (D == 128) ? SA2PP_WS_STAGES128 : SA2PP_WS_STAGES64;
   static constexpr int kQBytes = 128 * D;
   static constexpr int kKBytes = 64 * D;
   static constexpr int kVBytes = D * 64;
@@ -121,6 +124,9 @@ struct WsCfg {
   static_assert(128 * (kRegSoftmax + kRegPromote) <= kThreads * kRegLaunch,
                 "the warpgroups share the launch register budget");
   static_assert(2 * kSmemBytes <= 227 * 1024, "two CTAs per SM must fit in shared memory");
+  // block B's stage is refilled at issue iteration B - S + kNumPV (after the promotion of block
+  // B - S), and iteration j waits for block j + 2 before issuing S(j+2): B - S + kNumPV < B - 2
+  static_assert(kStages >= 3 + kNumPV, "too few K/V stages: the S(j+2) issue would wait for its own refill");
 };
 
 template <int N, typename OutT>
