@@ -172,9 +172,11 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
   // ---- work decode: grid = (n_qt, heads the unit range touches); CTA (x, y) is unit
   //      u = (b*Hq + h)*n_qt + qt of head bh = head0 + y, and exits unless u lies in [unit0, unit0 + units)
   //      (only the partial first/last heads of a q-tile shard have such CTAs); causal runs each head's
-  //      heaviest query tiles first
-  const int bh = p.head0 + static_cast<int>(blockIdx.y);
-  const int qt = CAUSAL ? (p.n_qt - 1 - static_cast<int>(blockIdx.x)) : static_cast<int>(blockIdx.x);
+  //      heaviest query tiles first -- with tile_major (small problems whose K/V fit in L2) the grid is
+  //      (heads, tiles) so every head's heaviest tile starts before any lighter one (LPT order)
+  const bool tm = CAUSAL && p.tile_major != 0;
+  const int bh = p.head0 + static_cast<int>(tm ? blockIdx.x : blockIdx.y);
+  const int qt = CAUSAL ? (p.n_qt - 1 - static_cast<int>(tm ? blockIdx.y : blockIdx.x)) : static_cast<int>(blockIdx.x);
   {
     const int u = bh * p.n_qt + qt;
     if (u < p.unit0 || u >= p.unit0 + p.units) return;
@@ -730,7 +732,7 @@ static cudaError_t launch_ws_t(const AttnParams& P, const sa2pp_quant& qt, cudaS
   if (e != cudaSuccess) return e;
   if (P.units <= 0) return cudaSuccess;
   const int h1 = (P.unit0 + P.units - 1) / P.n_qt;
-  dim3 grid(P.n_qt, h1 - P.head0 + 1);
+  const dim3 grid = (CAUSAL && P.tile_major) ? dim3(h1 - P.head0 + 1, P.n_qt) : dim3(P.n_qt, h1 - P.head0 + 1);
   kern<<<grid, C::kThreads, C::kSmemBytes, st>>>(mq, mk, mv, P);
   return cudaGetLastError();
 }

@@ -72,6 +72,7 @@ struct AttnParams {
   unsigned long long* trace;  // optional per-phase clock trace of a few CTAs (development aid)
   // query tiles [unit0, unit0 + units) of the flattened (b * Hq + h) * n_qt + qt space (one CTA each)
   int unit0, units, head0;  // head0 = unit0 / n_qt
+  int tile_major;           // causal grid order: 1 = (heads, tiles), all heads' heaviest tiles first
 };
 
 cudaError_t launch_prepass(const PrepassLaunch& L, cudaStream_t st);
