@@ -44,7 +44,7 @@ extern "C" {
 typedef enum {
   SA2PP_OK = 0,
   SA2PP_ERR_INVALID = 1,     /* bad shape, stride, pointer or config (reference: ValueError) */
-  SA2PP_ERR_UNSUPPORTED = 2, /* valid for the reference but not built here (e.g. head_dim 96) */
+  SA2PP_ERR_UNSUPPORTED = 2, /* valid for the reference but not built here (head_dim > 128) */
   SA2PP_ERR_RANGE = 3,       /* p_r * v_r above 2047/depth without waiver (RangeConfigError) */
   SA2PP_ERR_CUDA = 4         /* a CUDA runtime/driver call failed */
 } sa2pp_status;
@@ -59,7 +59,7 @@ typedef struct {
   int32_t heads_q;
   int32_t heads_kv;       /* heads_q % heads_kv == 0 (GQA); == heads_q for MHA */
   int32_t seq_len;        /* >= 1, any value (ragged tails handled as the reference pads) */
-  int32_t head_dim;       /* 64 or 128 */
+  int32_t head_dim;       /* 32, 64, 96 or 128 (32 / 96 run the 64 / 128 kernels on zero-padded channels) */
   int32_t causal;         /* 0 / 1 */
   int32_t smoothing;      /* 0 / 1  (attention.py:66, default 1) */
   int32_t qk_bits;        /* 8 (default) or 4: INT4 codes carried in INT8 containers */

@@ -60,10 +60,16 @@ def _problem(B, Hq, Hkv, N, D, *, causal, smoothing=True, qk_bits=8, pv_accum="f
                      float(p_r), float(v_r))
 
 
+def padded_dim(d: int) -> int:
+    """Kernel channel width for head_dim d (sa2pp_internal.h padded_dim): 32 -> 64, 96 -> 128."""
+    return 64 if d <= 64 else 128
+
+
 def alloc_quant(prob: A.Problem, device) -> QuantizedTensors:
     sz = A.QuantSizes()
     A.check(A.lib().sa2pp_quant_sizes(C_ref(prob), C_ref(sz)))
-    B, Hq, Hkv, N, D = prob.batch, prob.heads_q, prob.heads_kv, prob.seq_len, prob.head_dim
+    B, Hq, Hkv, N = prob.batch, prob.heads_q, prob.heads_kv, prob.seq_len
+    D = padded_dim(prob.head_dim)  # the kernels' channel width: head dims 32 / 96 run zero-padded
     n_qt, n_kb = -(-N // 128), -(-N // 64)
     nq_pad, np_ = n_qt * 128, n_kb * 64
     e = lambda *shape, dt: torch.empty(shape, dtype=dt, device=device)  # noqa: E731

@@ -129,13 +129,17 @@ struct WsCfg {
   static_assert(kStages >= 3 + kNumPV, "too few K/V stages: the S(j+2) issue would wait for its own refill");
 };
 
-template <int N, typename OutT>
-__device__ __forceinline__ void store_row(OutT* dst, const float2 (&O)[N / 2], float inv_l) {
+// MASKED: channels [d_out, N) are padding (head_dim 32 / 96 on the 64 / 128 kernels) and are not
+// stored.  Padded problems run the INSTR instantiation (its report/debug/trace hooks are null-guarded),
+// so the production kernel keeps its unmasked epilogue.
+template <int N, bool MASKED, typename OutT>
+__device__ __forceinline__ void store_row(OutT* dst, const float2 (&O)[N / 2], float inv_l, int d_out) {
   if constexpr (sizeof(OutT) == 4) {
 #pragma unroll
     for (int c = 0; c < N / 2; c += 2) {
-      *reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + 2 * c) =
-          make_float4(O[c].x * inv_l, O[c].y * inv_l, O[c + 1].x * inv_l, O[c + 1].y * inv_l);
+      if (!MASKED || 2 * c < d_out)
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(dst) + 2 * c) =
+            make_float4(O[c].x * inv_l, O[c].y * inv_l, O[c + 1].x * inv_l, O[c + 1].y * inv_l);
     }
   } else {
 #pragma unroll
@@ -152,7 +156,7 @@ __device__ __forceinline__ void store_row(OutT* dst, const float2 (&O)[N / 2], f
           w[i] = *reinterpret_cast<uint32_t*>(&h);
         }
       }
-      *reinterpret_cast<uint4*>(dst + 2 * c) = make_uint4(w[0], w[1], w[2], w[3]);
+      if (!MASKED || 2 * c < d_out) *reinterpret_cast<uint4*>(dst + 2 * c) = make_uint4(w[0], w[1], w[2], w[3]);
     }
   }
 }
@@ -669,7 +673,7 @@ __global__ void __launch_bounds__(WsCfg<D>::kThreads, 2)
       const float l = lbuf[r];
       const float inv_l = 1.0f / (l == 0.0f ? 1.0f : l);
       OutT* dst = reinterpret_cast<OutT*>(p.out) + b * p.o_sb + hq * p.o_sh + static_cast<int64_t>(row_g) * p.o_sn;
-      store_row<D, OutT>(dst, O, inv_l);
+      store_row<D, INSTR, OutT>(dst, O, inv_l, p.d_out);
     }
   }
 
@@ -749,7 +753,7 @@ static cudaError_t launch_ws_outi(const AttnParams& P, const sa2pp_quant& qt, cu
 
 template <int D, bool CAUSAL, bool ACC16, int G>
 static cudaError_t launch_ws_out(const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
-  if (P.debug != nullptr || P.report != nullptr || P.trace != nullptr)
+  if (P.debug != nullptr || P.report != nullptr || P.trace != nullptr || P.d_out < D)
     return launch_ws_outi<D, CAUSAL, ACC16, true, G>(P, qt, st);
   return launch_ws_outi<D, CAUSAL, ACC16, false, G>(P, qt, st);
 }
@@ -768,8 +772,8 @@ static cudaError_t launch_ws_d(const sa2pp_problem& prob, const AttnParams& P, c
 }
 
 cudaError_t launch_attn_ws(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st) {
-  if (prob.head_dim == 128) return launch_ws_d<128>(prob, P, qt, st);
-  if (prob.head_dim == 64) return launch_ws_d<64>(prob, P, qt, st);
+  if (padded_dim(prob.head_dim) == 128) return launch_ws_d<128>(prob, P, qt, st);
+  if (padded_dim(prob.head_dim) == 64) return launch_ws_d<64>(prob, P, qt, st);
   return cudaErrorInvalidValue;
 }
 

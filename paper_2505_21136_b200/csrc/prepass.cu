@@ -95,7 +95,7 @@ __device__ __forceinline__ void two_f64(const void* p, double& a, double& b) {
 
 template <typename T, int D>
 __global__ void __launch_bounds__(D / SA2PP_MEANS_CPT) channel_means_kernel(InView qv, InView kv, int Hq, int Hkv, int N,
-                                                              double* __restrict__ means) {
+                                                              double* __restrict__ means, int dc) {
   using M = MeansCfg<T, D>;
   extern __shared__ __align__(16) unsigned char ms_smem[];
   const int bh = blockIdx.x;  // in [0, B*(Hq+Hkv))
@@ -105,17 +105,24 @@ __global__ void __launch_bounds__(D / SA2PP_MEANS_CPT) channel_means_kernel(InVi
   const int hh = (h < Hq) ? h : h - Hq;
   const int t = threadIdx.x;
   const int n_st = (N + M::kRows - 1) / M::kRows;
+  // a thread's 16-byte pieces all sit at the same column of their rows, so the padded-channel
+  // test (head_dim 32 / 96) is one per thread
+  static_assert(M::kThreads % (M::kRowBytes / 16) == 0, "piece column must not depend on the piece");
+  const int c16 = t % (M::kRowBytes / 16);
+  const int col = c16 * (16 / static_cast<int>(sizeof(T))) < dc ? 16 * c16 : -1;
   auto issue = [&](int s) {
     if (s < n_st) {
       unsigned char* dst = ms_smem + (s % M::kStages) * M::kStageBytes;
 #pragma unroll
       for (int i = 0; i < M::kPieces; ++i) {
         const int piece = i * M::kThreads + t;  // 16-byte piece of the stage
-        const int r = piece / (M::kRowBytes / 16), c16 = piece % (M::kRowBytes / 16);
+        const int r = piece / (M::kRowBytes / 16);
         const int n = s * M::kRows + r;
-        const unsigned char* src = reinterpret_cast<const unsigned char*>(row_ptr<T>(v, b, hh, n < N ? n : 0)) + 16 * c16;
+        const bool ok = n < N && col >= 0;
+        const unsigned char* src =
+            reinterpret_cast<const unsigned char*>(row_ptr<T>(v, b, hh, n < N ? n : 0)) + (col >= 0 ? col : 0);
         const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst + 16 * piece));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(n < N ? 16 : 0) : "memory");
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0) : "memory");
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");  // empty groups keep the wait count uniform
@@ -287,7 +294,7 @@ template <typename T, int D>
 __global__ void __launch_bounds__(256, 2) quantize_q_kernel(InView qv, int Hq, int N, int Nq_pad, int n_qt, int n_tiles, int qmax,
                                                             const double* __restrict__ means, int Ht,
                                                             int8_t* __restrict__ q_codes, float* __restrict__ q_scale,
-                                                            double* __restrict__ q_scale64) {
+                                                            double* __restrict__ q_scale64, int dc) {
   constexpr int LPR = D / 8;      // lanes per row
   constexpr int RPP = 256 / LPR;  // row groups per CTA
   constexpr int RT = 128 / RPP;   // consecutive rows per thread (8 for D=128, 4 for D=64)
@@ -300,6 +307,7 @@ __global__ void __launch_bounds__(256, 2) quantize_q_kernel(InView qv, int Hq, i
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c8 = tid % LPR, rg = tid / LPR;
   const int c0 = c8 * 8;
+  const int qcol = c0 < dc ? c0 : -1;  // padded channels (head_dim 32 / 96) load as zeros
   auto prefetch = [&](int tile, int slot) {
     const int qt = tile % n_qt, bh = tile / n_qt;
     const int b = bh / Hq, h = bh % Hq;
@@ -307,10 +315,11 @@ __global__ void __launch_bounds__(256, 2) quantize_q_kernel(InView qv, int Hq, i
 #pragma unroll
     for (int rr = 0; rr < RT; ++rr) {
       const int r = n0 + rg * RT + rr;
-      const T* src = row_ptr<T>(qv, b, h, r < N ? r : 0) + c0;
+      const bool ok = r < N && qcol >= 0;
+      const T* src = row_ptr<T>(qv, b, h, r < N ? r : 0) + (qcol >= 0 ? qcol : 0);
 #pragma unroll
       for (int u = 0; u < NW; ++u)
-        cp_async16<T>(&stage[(slot * SLOT + rr * NW + u) * 256 + tid], reinterpret_cast<const uint4*>(src) + u, r < N);
+        cp_async16<T>(&stage[(slot * SLOT + rr * NW + u) * 256 + tid], reinterpret_cast<const uint4*>(src) + u, ok);
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -512,13 +521,15 @@ __device__ __forceinline__ void load_rows(const InView& in, int b, int h, int n0
 #ifndef SA2PP_K_MINB
 #define SA2PP_K_MINB 3
 #endif
-template <typename T, int D>
+// PAD: head_dim < D (32 / 96), threads of the padded channels load nothing (zeros); a separate
+// instantiation so the unpadded kernel keeps its register allocation
+template <typename T, int D, bool PAD>
 __global__ void __launch_bounds__(256, SA2PP_K_MINB) quantize_k_kernel(InView kv_in, int Hq, int Hkv, int N, int Np, int n_kb,
                                                             int qmax, int smoothing, double sm_scale_log2,
                                                             const double* __restrict__ means, int Ht,
                                                             int8_t* __restrict__ k_codes, float* __restrict__ kv_meta,
                                                             double* __restrict__ kv_scale64, float* __restrict__ bias,
-                                                            float* __restrict__ bias_l2) {
+                                                            float* __restrict__ bias_l2, int dc) {
   using G = KvGeom<T, D>;
   constexpr int LPR = G::LPR, RT = G::RT;
   __shared__ float s_kmn[8 * D], s_kmx[8 * D];
@@ -533,7 +544,7 @@ __global__ void __launch_bounds__(256, SA2PP_K_MINB) quantize_k_kernel(InView kv
   const int c0 = c8 * 8;
 
   KvTile<T> kt[RT];  // rows past N are zero (padding after smoothing)
-  load_rows<T, D>(kv_in, b, h, n0, rg, c0, rows, kt);
+  load_rows<T, D>(kv_in, b, h, n0, rg, c0, PAD && c0 >= dc ? 0 : rows, kt);
   const double* kmu_g = means + (static_cast<int64_t>(b) * Ht + Hq + h) * D;
 
   // ---- per-channel min/max over the block's valid rows
@@ -724,10 +735,10 @@ __host__ __device__ constexpr int v_smem_bytes() {
 #ifndef SA2PP_V_MINB
 #define SA2PP_V_MINB 4
 #endif
-template <typename T, int D>
+template <typename T, int D, bool PAD>
 __global__ void __launch_bounds__(256, SA2PP_V_MINB) quantize_v_kernel(InView v_in, int Hkv, int N, int Np, int n_kb, double v_r,
                                                             uint8_t* __restrict__ v_codes, float* __restrict__ kv_meta,
-                                                            double* __restrict__ kv_scale64) {
+                                                            double* __restrict__ kv_scale64, int dc) {
   using G = KvGeom<T, D>;
   constexpr int LPR = G::LPR, RT = G::RT, UPR = G::UPR;
   extern __shared__ __align__(16) unsigned char v_smem[];
@@ -745,7 +756,7 @@ __global__ void __launch_bounds__(256, SA2PP_V_MINB) quantize_v_kernel(InView v_
   const int c0 = c8 * 8;
 
   KvTile<T> vt[RT];  // rows past N are zero (the reference pads V with zeros)
-  load_rows<T, D>(v_in, b, h, n0, rg, c0, rows, vt);
+  load_rows<T, D>(v_in, b, h, n0, rg, c0, PAD && c0 >= dc ? 0 : rows, vt);
 
   // ---- per-channel |max| over the block (zero rows do not change it)
   {
@@ -830,7 +841,7 @@ __global__ void __launch_bounds__(256, SA2PP_V_MINB) quantize_v_kernel(InView v_
       const int bit = __ffs(tmask) - 1;
       tmask &= tmask - 1u;
       const int i = bit / RT, rr = bit % RT, c = c0 + i;
-      const float x = to_f32<T>(row_ptr<T>(v_in, b, h, n0 + rg * RT + rr)[c]);
+      const float x = !PAD || c < dc ? to_f32<T>(row_ptr<T>(v_in, b, h, n0 + rg * RT + rr)[c]) : 0.0f;
       s_vt[c * 64 + (rg ^ swz) * RT + rr] = v_code_exact(x, s_vsc[c]);
     }
   }
@@ -903,17 +914,24 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
   {
     static PerDevice v_once;
     cudaError_t e = v_once.run([&](std::atomic<int>&) {
-      return cudaFuncSetAttribute(quantize_v_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, v_smem);
+      cudaError_t r = cudaFuncSetAttribute(quantize_v_kernel<T, D, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           v_smem);
+      if (r == cudaSuccess)
+        r = cudaFuncSetAttribute(quantize_v_kernel<T, D, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, v_smem);
+      return r;
     });
     if (e != cudaSuccess) return e;
   }
+  const bool pad = L.d_in < D;
+  const auto vk = pad ? quantize_v_kernel<T, D, true> : quantize_v_kernel<T, D, false>;
+  const auto kk = pad ? quantize_k_kernel<T, D, true> : quantize_k_kernel<T, D, false>;
   SideStream& side = side_stream();
   if (side.stream != nullptr) {
     cudaError_t e = cudaEventRecord(side.fork, st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(side.stream, side.fork, 0);
     if (e != cudaSuccess) return e;
-    quantize_v_kernel<T, D><<<gk, 256, v_smem, side.stream>>>(vv, L.Hkv, L.N, L.Np, L.n_kb, L.v_r, L.v_codes,
-                                                              L.kv_meta, L.kv_scale64);
+    vk<<<gk, 256, v_smem, side.stream>>>(vv, L.Hkv, L.N, L.Np, L.n_kb, L.v_r, L.v_codes,
+                                                              L.kv_meta, L.kv_scale64, L.d_in);
   }
   if (L.smoothing) {
     using M = MeansCfg<T, D>;
@@ -923,7 +941,7 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
       return cudaFuncSetAttribute(channel_means_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     });
     if (e != cudaSuccess) return e;
-    channel_means_kernel<T, D><<<L.B * Ht, M::kThreads, smem, st>>>(qv, kv, L.Hq, L.Hkv, L.N, L.means);
+    channel_means_kernel<T, D><<<L.B * Ht, M::kThreads, smem, st>>>(qv, kv, L.Hq, L.Hkv, L.N, L.means, L.d_in);
   } else {
     cudaMemsetAsync(L.means, 0, sizeof(double) * L.B * Ht * D, st);
   }
@@ -945,17 +963,17 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
     const int n_tiles = L.n_qt * L.B * L.Hq;
     const int grid = n_tiles < sms * ctas_per_sm ? n_tiles : sms * ctas_per_sm;
     quantize_q_kernel<T, D><<<grid, 256, q_smem, st>>>(qv, L.Hq, L.N, L.Nq_pad, L.n_qt, n_tiles, L.qmax, L.means, Ht,
-                                                       L.q_codes, L.q_scale, L.q_scale64);
+                                                       L.q_codes, L.q_scale, L.q_scale64, L.d_in);
   }
-  quantize_k_kernel<T, D><<<gk, 256, 0, st>>>(kv, L.Hq, L.Hkv, L.N, L.Np, L.n_kb, L.qmax, L.smoothing, L.sm_scale_log2,
-                                              L.means, Ht, L.k_codes, L.kv_meta, L.kv_scale64, L.bias, L.bias_l2);
+  kk<<<gk, 256, 0, st>>>(kv, L.Hq, L.Hkv, L.N, L.Np, L.n_kb, L.qmax, L.smoothing, L.sm_scale_log2,
+                                              L.means, Ht, L.k_codes, L.kv_meta, L.kv_scale64, L.bias, L.bias_l2, L.d_in);
   if (side.stream != nullptr) {  // join: the caller's stream waits for quantize_v
     cudaError_t e = cudaEventRecord(side.join, side.stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(st, side.join, 0);
     if (e != cudaSuccess) return e;
   } else {
-    quantize_v_kernel<T, D><<<gk, 256, v_smem, st>>>(vv, L.Hkv, L.N, L.Np, L.n_kb, L.v_r, L.v_codes, L.kv_meta,
-                                                     L.kv_scale64);
+    vk<<<gk, 256, v_smem, st>>>(vv, L.Hkv, L.N, L.Np, L.n_kb, L.v_r, L.v_codes, L.kv_meta,
+                                                     L.kv_scale64, L.d_in);
   }
   return cudaGetLastError();
 }
@@ -987,12 +1005,12 @@ __global__ void report_init_kernel(sa2pp_report* r) {
 }
 
 // Positive doubles order like their bit patterns, so 64-bit integer atomics give FP64 min/max.
-__global__ void vscale_minmax_kernel(const double* __restrict__ s, int64_t blocks, int D, sa2pp_report* r) {
+__global__ void vscale_minmax_kernel(const double* __restrict__ s, int64_t blocks, int D, int d, sa2pp_report* r) {
   unsigned long long mn = 0x7ff0000000000000ull, mx = 0ull;
-  const int64_t n = blocks * D;
+  const int64_t n = blocks * d;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const unsigned long long b = __double_as_longlong(s[(i / D) * (1 + D) + 1 + i % D]);
+    const unsigned long long b = __double_as_longlong(s[(i / d) * (1 + D) + 1 + i % d]);
     mn = b < mn ? b : mn;
     mx = b > mx ? b : mx;
   }
@@ -1012,10 +1030,11 @@ cudaError_t launch_report_init(sa2pp_report* r, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_vscale_minmax(const double* kv_scale64, int64_t blocks, int D, sa2pp_report* r, cudaStream_t st) {
-  const int64_t n = blocks * D;
+cudaError_t launch_vscale_minmax(const double* kv_scale64, int64_t blocks, int D, int d, sa2pp_report* r,
+                                 cudaStream_t st) {
+  const int64_t n = blocks * d;
   const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 1184));
-  vscale_minmax_kernel<<<grid, 256, 0, st>>>(kv_scale64, blocks, D, r);
+  vscale_minmax_kernel<<<grid, 256, 0, st>>>(kv_scale64, blocks, D, d, r);
   return cudaGetLastError();
 }
 

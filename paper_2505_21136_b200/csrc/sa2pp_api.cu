@@ -123,8 +123,8 @@ int sa2pp_check_problem(const sa2pp_problem* p) {
     return fail(SA2PP_ERR_INVALID, "heads_q (%d) must be a multiple of heads_kv (%d)", p->heads_q, p->heads_kv);
   if (p->head_dim % 32 != 0)  // attention.py:242-243
     return fail(SA2PP_ERR_INVALID, "head_dim must be a multiple of 32 for the FP8 path");
-  if (p->head_dim != 64 && p->head_dim != 128)
-    return fail(SA2PP_ERR_UNSUPPORTED, "head_dim %d not built (64, 128)", p->head_dim);
+  if (p->head_dim > 128)
+    return fail(SA2PP_ERR_UNSUPPORTED, "head_dim %d not built (32, 64, 96, 128)", p->head_dim);
   if (p->qk_bits != 8 && p->qk_bits != 4) return fail(SA2PP_ERR_INVALID, "qk_bits must be 4 or 8");
   if (p->pv_accum != SA2PP_ACC_F16 && p->pv_accum != SA2PP_ACC_F32)
     return fail(SA2PP_ERR_INVALID, "pv_accumulator must be fp16 or fp32");
@@ -146,7 +146,7 @@ int sa2pp_quant_sizes(const sa2pp_problem* p, sa2pp_quant_sizes_t* s) {
   if (rc) return rc;
   if (!s) return fail(SA2PP_ERR_INVALID, "sizes is NULL");
   const Dims d = dims_of(*p);
-  const int64_t B = p->batch, Hq = p->heads_q, Hkv = p->heads_kv, D = p->head_dim;
+  const int64_t B = p->batch, Hq = p->heads_q, Hkv = p->heads_kv, D = sa2pp::padded_dim(p->head_dim);
   s->q_codes = B * Hq * d.nq_pad * D;
   s->q_scale = B * Hq * d.n_qt * 4;
   s->q_scale64 = B * Hq * d.n_qt * 8;
@@ -200,7 +200,8 @@ int sa2pp_prepass(const sa2pp_problem* p, const sa2pp_inputs* in, const sa2pp_qu
   const Dims d = dims_of(*p);
   sa2pp::PrepassLaunch L{};
   L.dtype = in->dtype;
-  L.D = p->head_dim;
+  L.D = sa2pp::padded_dim(p->head_dim);
+  L.d_in = p->head_dim;
   L.B = p->batch;
   L.Hq = p->heads_q;
   L.Hkv = p->heads_kv;
@@ -275,6 +276,7 @@ int sa2pp_attn_fwd_units(const sa2pp_problem* p, const sa2pp_quant* qt, const sa
   P.o_sb = out->o_stride[0];
   P.o_sh = out->o_stride[1];
   P.o_sn = out->o_stride[2];
+  P.d_out = p->head_dim;
   P.report = report;
   P.debug = g_debug;
   P.trace = g_trace;
@@ -290,13 +292,13 @@ int sa2pp_attn_fwd_units(const sa2pp_problem* p, const sa2pp_quant* qt, const sa
   // while the K/V codes stay within ~2.4x the 126 MB L2: measured +10-15 % at 1K-2K, +3-7 % at 4K-8K
   // and for Llama GQA 8K; beyond that the head-major order's K/V reuse between neighbouring CTAs wins
   // (16K D=128: 791 vs 862 TOPS tile-major vs head-major)
-  const double kv_bytes = static_cast<double>(p->batch) * p->heads_kv * d.np * p->head_dim * 2.0;
+  const double kv_bytes = static_cast<double>(p->batch) * p->heads_kv * d.np * sa2pp::padded_dim(p->head_dim) * 2.0;
   P.tile_major = (p->causal && kv_bytes <= 300e6) ? 1 : 0;
   cudaError_t e = sa2pp::launch_attn_ws(*p, P, *qt, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "attention launch");
   if (report != nullptr) {  // v_scale min/max over every (key block, channel) (attention.py:271-275)
-    e = sa2pp::launch_vscale_minmax(qt->kv_scale64, static_cast<int64_t>(p->batch) * p->heads_kv * d.n_kb, p->head_dim,
-                                    report, static_cast<cudaStream_t>(stream));
+    e = sa2pp::launch_vscale_minmax(qt->kv_scale64, static_cast<int64_t>(p->batch) * p->heads_kv * d.n_kb,
+                                    sa2pp::padded_dim(p->head_dim), p->head_dim, report, static_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "report launch");
   }
   return SA2PP_OK;

@@ -39,7 +39,13 @@ struct PerDevice {
   }
 };
 
+// Head dims 32 and 96 run the 64 / 128 kernels on zero-padded channels: the loaders read d_in
+// channels and supply zeros for the rest, which leaves every scale, code, bias and output channel
+// of the real ones unchanged (per-block amax over zeros, per-channel V scales, independent PV columns).
+__host__ __device__ constexpr int padded_dim(int d) { return d <= 64 ? 64 : 128; }
+
 struct PrepassLaunch {
+  int d_in;  // channels present in the inputs (head_dim); D is the padded kernel width
   int dtype, D, B, Hq, Hkv, N, Nq_pad, Np, n_qt, n_kb, qmax, smoothing;
   double v_r, sm_scale_log2;
   const void *q, *k, *v;
@@ -67,6 +73,7 @@ struct AttnParams {
   const float* bias_l2;
   void* out;
   int64_t o_sb, o_sh, o_sn;
+  int d_out;  // channels written to out (head_dim <= the kernel's D)
   sa2pp_report* report;
   uint32_t* debug;
   unsigned long long* trace;  // optional per-phase clock trace of a few CTAs (development aid)
@@ -78,8 +85,10 @@ struct AttnParams {
 cudaError_t launch_prepass(const PrepassLaunch& L, cudaStream_t st);
 cudaError_t launch_attn_ws(const sa2pp_problem& prob, const AttnParams& P, const sa2pp_quant& qt, cudaStream_t st);
 cudaError_t launch_report_init(sa2pp_report* r, cudaStream_t st);
-// min/max of the FP64 V scales [blocks][1 + D] (column 0 is dK) into report->v_scale_{min,max}_bits
-cudaError_t launch_vscale_minmax(const double* kv_scale64, int64_t blocks, int D, sa2pp_report* r, cudaStream_t st);
+// min/max of the FP64 V scales [blocks][1 + D] (column 0 is dK) over the first d channels into
+// report->v_scale_{min,max}_bits
+cudaError_t launch_vscale_minmax(const double* kv_scale64, int64_t blocks, int D, int d, sa2pp_report* r,
+                                 cudaStream_t st);
 
 // 2-D uint8 TMA map (inner extent `inner` bytes, `rows` rows of `row_bytes`), box box_inner x box_rows.
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,

@@ -164,3 +164,6 @@ if __name__ == "__main__":
     case("depth1_d128", 1, 192, 128, seed=19, rng_cfg=(448.0, 4.5, 1, False))
     case("seq1_d64", 1, 1, 64, seed=20)
     case("scale_d128", 1, 256, 128, seed=21, softmax_scale=0.05, rng_cfg=(112.0, 9.0, 2, False))
+    # head dims 32 (the reference's own test dim) and 96: zero-padded channels on the 64/128 kernels
+    case("d32", 2, 256, 32, seed=22)
+    case("ragged_causal_d96", 1, 200, 96, seed=23, causal=True)

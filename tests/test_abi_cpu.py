@@ -48,11 +48,22 @@ def test_valid_problem():
     assert rc() == A.SA2PP_OK
     assert rc(D=128, Hq=32, Hkv=8) == A.SA2PP_OK
     assert rc(N=1) == A.SA2PP_OK and rc(N=17776) == A.SA2PP_OK
+    assert rc(D=32) == A.SA2PP_OK and rc(D=96, Hq=4, Hkv=2) == A.SA2PP_OK  # zero-padded to 64 / 128
+
+
+def test_quant_sizes_of_padded_head_dims():
+    """head_dim 32 / 96 quantize into the 64 / 128-channel layout the kernels read."""
+    for d, dp in ((32, 64), (96, 128)):
+        prob = _problem(1, 2, 2, 1000, d, causal=False)
+        sz = A.QuantSizes()
+        assert A.lib().sa2pp_quant_sizes(ctypes.byref(prob), ctypes.byref(sz)) == 0
+        assert sz.k_codes == 2 * 16 * 64 * dp and sz.means == 2 * 2 * dp * 8
+        assert sz.kv_scale64 == 2 * 16 * (1 + dp) * 8
 
 
 @pytest.mark.parametrize("kw,code", [
     (dict(D=48), A.SA2PP_ERR_INVALID),            # not a multiple of 32 (attention.py:242-243)
-    (dict(D=96), A.SA2PP_ERR_UNSUPPORTED),        # valid for the reference, not built here
+    (dict(D=160), A.SA2PP_ERR_UNSUPPORTED),       # valid for the reference, not built here
     (dict(Hq=6, Hkv=4), A.SA2PP_ERR_INVALID),     # GQA group must divide
     (dict(N=0), A.SA2PP_ERR_INVALID),
     (dict(qk_bits=6), A.SA2PP_ERR_INVALID),       # attention.py:82-83

@@ -8,6 +8,8 @@ Bar (DESIGN.md "Parity"):
     L1 <= (reference's own L1 vs exact) + 1e-3.
 """
 
+import math
+
 import numpy as np
 import pytest
 
@@ -22,7 +24,7 @@ if not gpu_ready():
 import paper_2505_21136_b200 as sa  # noqa: E402
 from oracle import sage_cpu as oc  # noqa: E402
 
-SUPPORTED = [n for n in golden_cases() if golden_config(load_golden(n))["dim"] in (64, 128)]
+SUPPORTED = [n for n in golden_cases() if golden_config(load_golden(n))["dim"] in (32, 64, 96, 128)]
 
 
 def run_case(g, dtype=torch.float32, layout="HND"):
@@ -49,23 +51,30 @@ def f32_ulp_close(a32, b64):
 
 @pytest.mark.parametrize("name", SUPPORTED)
 def test_prepass_bit_exact(name):
+    """Head dims 32 / 96 run the 64 / 128 kernels on zero-padded channels: the real channels must
+    match the reference bit for bit and every padded one must be zero."""
     g = load_golden(name)
     c = golden_config(g)
-    n = c["seq"]
+    n, d = c["seq"], c["dim"]
     _, qt, _ = run_case(g)
     qc = qt.q_codes[0].cpu().numpy()
-    assert np.array_equal(qc[:, :n], g["q_codes"]), "Q INT8 codes"
+    assert np.array_equal(qc[:, :n, :d], g["q_codes"]), "Q INT8 codes"
     assert not qc[:, n:].any(), "Q pad rows must be zero"
+    assert not qc[..., d:].any(), "Q pad channels must be zero"
     assert np.array_equal(qt.q_scale64[0].cpu().numpy(), g["q_scale"]), "Q scales (f64)"
     assert np.array_equal(qt.q_scale[0].cpu().numpy(), g["q_scale"].astype(np.float32)), "Q scales (f32)"
-    assert np.array_equal(qt.k_codes[0].cpu().numpy(), g["k_codes"]), "K INT8 codes"
+    kc = qt.k_codes[0].cpu().numpy()
+    assert np.array_equal(kc[..., :d], g["k_codes"]), "K INT8 codes"
+    assert not kc[..., d:].any(), "K pad channels must be zero"
     assert np.array_equal(qt.k_scale64[0].cpu().numpy(), g["k_scale"]), "K scales"
     vt = qt.v_codes[0].cpu().numpy().transpose(0, 2, 1)
-    assert np.array_equal(vt, g["v_codes"]), "V E4M3 codes"
-    assert np.array_equal(qt.v_scale64[0].cpu().numpy(), g["v_scale"]), "V scales"
+    assert np.array_equal(vt[..., :d], g["v_codes"]), "V E4M3 codes"
+    assert not vt[..., d:].any(), "V pad channels must be zero"
+    assert np.array_equal(qt.v_scale64[0].cpu().numpy()[..., :d], g["v_scale"]), "V scales"
     means = qt.means[0].cpu().numpy()
-    assert np.array_equal(means[: c["heads"]], g["q_mean"]), "Q means"
-    assert np.array_equal(means[c["heads"]:], g["k_mean"]), "K means"
+    assert np.array_equal(means[: c["heads"], :d], g["q_mean"]), "Q means"
+    assert np.array_equal(means[c["heads"]:, :d], g["k_mean"]), "K means"
+    assert not means[:, d:].any(), "pad channel means must be zero"
     assert f32_ulp_close(qt.bias[0].cpu().numpy(), g["bias"]), "bias within 1 ulp f32"
 
 
@@ -121,10 +130,13 @@ def test_qk_scores_exact_in_tmem():
     assert np.array_equal(s, want)
 
 
-def test_reference_mirror_run_report():
-    g = load_golden("attn_oracle")
+@pytest.mark.parametrize("name", ["attn_oracle", "attn_d32", "attn_ragged_causal_d96"])
+def test_reference_mirror_run_report(name):
+    """Every RunReport field against the reference's, including the V-scale range, which must not
+    see the padded channels of head dims 32 / 96."""
+    g = load_golden(name)
     c = golden_config(g)
-    cfg = sa.AttentionConfig(seq_len=c["seq"], head_dim=c["dim"], num_heads=c["heads"])
+    cfg = sa.AttentionConfig(seq_len=c["seq"], head_dim=c["dim"], num_heads=c["heads"], causal=c["causal"])
     rep = sa.attention_quantized(g["q"], g["k"], g["v"], cfg)
     assert rep.mma_invocations == int(g["mma"])
     assert rep.fp16_to_fp32_conversions == int(g["conversions"])
@@ -397,9 +409,12 @@ def test_nhd_strided_views_and_fp16():
 
 
 def test_rejects_unsupported_inputs():
-    q = torch.randn(1, 2, 64, 96, device="cuda")
+    q = torch.randn(1, 2, 64, 160, device="cuda")
     with pytest.raises(ValueError):
-        sa.sageattn(q, q, q)  # head_dim 96 is not built
+        sa.sageattn(q, q, q)  # head_dim 160 is not built (32, 64, 96, 128 are)
+    q = torch.randn(1, 2, 64, 48, device="cuda")
+    with pytest.raises(ValueError):
+        sa.sageattn(q, q, q)  # not a multiple of 32 (attention.py:242-243)
     with pytest.raises(ValueError):
         sa.sageattn(q.cpu(), q.cpu(), q.cpu())  # no CPU fallback
     q = torch.randn(1, 6, 64, 64, device="cuda")
@@ -427,14 +442,16 @@ def _integration_stub():
     return ns
 
 
-def test_integration_stub_run_report_matches_reference_counters():
+@pytest.mark.parametrize("D", [64, 32, 96])
+def test_integration_stub_run_report_matches_reference_counters(D):
     """The INTEGRATION.md binding (numpy in, numpy + RunReport out through
     sa2pp_host_pipeline_run_report) against the unmodified reference on the same inputs: every
-    counter of lpattn's RunReport (attention.py:114-125), output within the parity bar."""
+    counter of lpattn's RunReport (attention.py:114-125), output within the parity bar.  Head dims
+    32 / 96 run zero-padded on the 64 / 128 kernels."""
     ns = _integration_stub()
     import lpattn
     rng = np.random.Generator(np.random.Philox(21))
-    H, N, D = 2, 320, 64
+    H, N = 2, 320
     q, k, v = (rng.standard_normal((H, N, D)).astype(np.float32) for _ in range(3))
     cfg = lpattn.AttentionConfig(seq_len=N, head_dim=D, num_heads=H, causal=True)
     got = ns["attention_quantized"](q, k, v, cfg)
@@ -464,6 +481,30 @@ def test_integration_stub_reports_fp16_overflow():
     assert got.overflow_events > 0 and got.overflow_events == dev.overflow_events
     assert (got.p_scale_min, got.p_scale_max) == (dev.p_scale_min, dev.p_scale_max)
     assert (got.v_scale_min, got.v_scale_max) == (dev.v_scale_min, dev.v_scale_max)
+
+
+@pytest.mark.parametrize("d", [32, 96])
+def test_padded_head_dims_nhd_gqa_bf16(d):
+    """head_dim 32 / 96 through sageattn on strided NHD bf16 GQA inputs: only the d real channels
+    are written (the output row stride is d), causal and not, against SDPA and a zero-padded run of
+    the 64 / 128 kernel."""
+    g = torch.Generator(device="cuda").manual_seed(d)
+    q = torch.randn(2, 333, 8, d, device="cuda", generator=g).bfloat16()
+    k, v = (torch.randn(2, 333, 2, d, device="cuda", generator=g).bfloat16() for _ in range(2))
+    dp = 64 if d <= 64 else 128
+    pad = lambda t: torch.nn.functional.pad(t, (0, dp - d))  # noqa: E731
+    for causal in (False, True):
+        o = sa.sageattn(q, k, v, "NHD", causal)
+        assert o.shape == q.shape
+        # the padded run computes the same codes; its sm_scale is the real head dim's
+        o_pad = sa.sageattn(pad(q), pad(k), pad(v), "NHD", causal, 1.0 / math.sqrt(d))
+        torch.cuda.synchronize()
+        assert torch.equal(o, o_pad[..., :d])
+        qf, kf, vf = (t.transpose(1, 2).float() for t in (q, k, v))
+        kf, vf = (t.repeat_interleave(4, dim=1) for t in (kf, vf))
+        ref = torch.nn.functional.scaled_dot_product_attention(qf, kf, vf, is_causal=causal)
+        cos, _, _ = sa.compare(ref.transpose(1, 2).double().cpu().numpy(), o.double().cpu().numpy())
+        assert cos >= 0.999, (d, causal, cos)
 
 
 def test_torch_library_op():

@@ -1,9 +1,8 @@
 """The reference's own operator tests (lpattn tests/test_attention.py:173-265, class TestQuantized),
 run through the B200 `attention_quantized` mirror with the same assertions.
 
-The reference uses head_dim 32 there; the sm_100a kernels are built for head_dim 64 and 128
-(SA2PP_ERR_UNSUPPORTED otherwise), so the cases run at 64 with the reference's seeds,
-shapes and thresholds otherwise unchanged.  Buffering depth 1 with the FP16 accumulator runs each
+The cases run at the reference's head_dim 32 (the 64-channel kernels on zero-padded channels) with
+its seeds, shapes and thresholds unchanged.  Buffering depth 1 with the FP16 accumulator runs each
 k=32 group as its own tcgen05 MMA into a fresh FP16 accumulator, converted and promoted on its own.
 """
 
@@ -21,7 +20,7 @@ if not gpu_ready():
 import paper_2505_21136_b200 as sa  # noqa: E402
 from oracle import sage_cpu as oc  # noqa: E402
 
-D = 64
+D = 32  # tests/test_attention.py uses head_dim 32
 
 
 def gaussian_qkv(seed, heads, n, d):
