@@ -861,9 +861,13 @@ __global__ void __launch_bounds__(256, SA2PP_V_MINB) quantize_v_kernel(InView v_
 // ------------------------------------------------------------------ host launcher
 // A non-blocking side stream and its fork/join events, per calling thread and device (created on
 // first use, destroyed with the thread); nullptr stream = run everything on the caller's stream.
+#ifndef SA2PP_Q_SIDE_MAXN
+#define SA2PP_Q_SIDE_MAXN 2048  // quantize_q beside quantize_k up to this sequence length
+#endif
+
 struct SideStream {
   cudaStream_t stream = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, mid = nullptr;
   int dev = -1;
   ~SideStream() {
     if (stream != nullptr) {
@@ -871,6 +875,7 @@ struct SideStream {
       if (cudaGetDevice(&cur) == cudaSuccess && cur != dev) cudaSetDevice(dev);
       cudaEventDestroy(fork);
       cudaEventDestroy(join);
+      cudaEventDestroy(mid);
       cudaStreamDestroy(stream);
       if (cur != dev) cudaSetDevice(cur);
     }
@@ -889,7 +894,8 @@ static SideStream& side_stream() {
       return none;
     }
     if (cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess) {
+        cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s.mid, cudaEventDisableTiming) != cudaSuccess) {
       cudaStreamDestroy(s.stream);
       s.stream = nullptr;
       return none;
@@ -962,7 +968,16 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
     const int ctas_per_sm = occ.get();
     const int n_tiles = L.n_qt * L.B * L.Hq;
     const int grid = n_tiles < sms * ctas_per_sm ? n_tiles : sms * ctas_per_sm;
-    quantize_q_kernel<T, D><<<grid, 256, q_smem, st>>>(qv, L.Hq, L.N, L.Nq_pad, L.n_qt, n_tiles, L.qmax, L.means, Ht,
+    // short sequences: quantize_q joins quantize_v on the side stream once the means are done, so
+    // it runs beside quantize_k (each is a few latency-bound waves there; at 4K+ they contend)
+    cudaStream_t qs = st;
+    if (side.stream != nullptr && L.N <= SA2PP_Q_SIDE_MAXN) {
+      e = cudaEventRecord(side.mid, st);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(side.stream, side.mid, 0);
+      if (e != cudaSuccess) return e;
+      qs = side.stream;
+    }
+    quantize_q_kernel<T, D><<<grid, 256, q_smem, qs>>>(qv, L.Hq, L.N, L.Nq_pad, L.n_qt, n_tiles, L.qmax, L.means, Ht,
                                                        L.q_codes, L.q_scale, L.q_scale64, L.d_in);
   }
   kk<<<gk, 256, 0, st>>>(kv, L.Hq, L.Hkv, L.N, L.Np, L.n_kb, L.qmax, L.smoothing, L.sm_scale_log2,
