@@ -5,6 +5,8 @@
 tag=${1:-san}
 out=gpurun_out/$tag
 mkdir -p $out
+# no caching allocator: each tensor is its own cudaMalloc, so memcheck sees accesses past its end
+export PYTORCH_NO_CUDA_MEMORY_CACHING=1
 for tool in memcheck racecheck synccheck initcheck; do
   extra=""
   [ $tool = racecheck ] && extra="--racecheck-report all"

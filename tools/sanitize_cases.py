@@ -1,10 +1,13 @@
 """Small sageattn invocations for compute-sanitizer (racecheck / synccheck / memcheck / initcheck).
 
-Covers both head dims, causal and non-causal, a ragged tail (N % 64 != 0 and N % 128 != 0),
+Covers head dims 32 / 64 / 96 / 128 (32 and 96 zero-padded onto the 64 / 128 kernels), causal and non-causal, a ragged tail (N % 64 != 0 and N % 128 != 0),
 GQA, FP16 and FP32 PV accumulation and the instrumented (RunReport) kernel variant, at small
 B*H so the sanitizer's serialisation stays within minutes.  Exits non-zero on a CUDA error.
 
     compute-sanitizer --tool racecheck python tools/sanitize_cases.py
+
+Run memcheck/initcheck with PYTORCH_NO_CUDA_MEMORY_CACHING=1 so every tensor is its own allocation
+and an out-of-bounds access past a tensor's end is reported (tools/gpu_sanitize.sh does).
 """
 
 from __future__ import annotations
@@ -27,6 +30,8 @@ CASES = [
     (1, 1, 1, 1100, 128, False, "fp32"),
     (1, 1, 1, 17776 // 8, 64, False, "fp16"),  # the CogVideoX ragged tail (48 real keys in the last block)
     (1, 2, 2, 640, 128, False, "fp16-depth1"),  # buffering depth 1: each k=32 group its own FP16 accumulation
+    (1, 2, 1, 333, 32, True, "fp16"),   # head_dim 32 on the 64 kernel: padded-channel loads and stores
+    (1, 2, 2, 1000, 96, False, "fp16"),  # head_dim 96 on the 128 kernel
 ]
 
 
