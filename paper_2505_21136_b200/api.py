@@ -172,7 +172,7 @@ class HostPipeline:
     """
 
     def __init__(self, B, Hq, Hkv, N, D, dtype=torch.bfloat16, device="cuda", *, is_causal=False,
-                 sm_scale=None, pv_accum="fp16", chunks=16, depth=3, **kw):
+                 sm_scale=None, pv_accum="fp16", chunks=8, depth=3, **kw):
         if Hq % Hkv:
             raise ValueError("heads_q must be a multiple of heads_kv")
         if dtype not in _DT:
@@ -225,7 +225,7 @@ class HostPipeline:
 
 
 def sageattn_host(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, is_causal: bool = False,
-                  sm_scale: Optional[float] = None, *, out: Optional[torch.Tensor] = None, chunks: int = 16,
+                  sm_scale: Optional[float] = None, *, out: Optional[torch.Tensor] = None, chunks: int = 8,
                   **kw) -> torch.Tensor:
     """One-shot `HostPipeline` call: pinned HND host tensors in, pinned host output out."""
     B, Hq, N, D = q.shape
