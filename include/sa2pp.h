@@ -111,7 +111,8 @@ typedef struct {
 
 typedef struct {
   size_t q_codes, q_scale, q_scale64, k_codes, v_codes, kv_meta, kv_scale64, bias, bias_l2, means;
-  size_t workspace; /* reserved scratch (0 bytes with the current kernels) */
+  size_t workspace; /* prepass scratch for the parallel exact channel means; a smaller or NULL workspace
+                       selects the sequential mean kernel (same bits, slower) */
 } sa2pp_quant_sizes_t;
 
 /* Output [.., D] with element strides for (batch, head, token), same dtype choices as inputs. */

@@ -95,10 +95,12 @@ __device__ __forceinline__ void two_f64(const void* p, double& a, double& b) {
 
 template <typename T, int D>
 __global__ void __launch_bounds__(D / SA2PP_MEANS_CPT) channel_means_kernel(InView qv, InView kv, int Hq, int Hkv, int N,
-                                                              double* __restrict__ means, int dc) {
+                                                              double* __restrict__ means, int dc,
+                                                              const int* __restrict__ need) {
   using M = MeansCfg<T, D>;
   extern __shared__ __align__(16) unsigned char ms_smem[];
   const int bh = blockIdx.x;  // in [0, B*(Hq+Hkv))
+  if (need != nullptr && need[bh] == 0) return;  // the parallel path's certificate held for this head
   const int Ht = Hq + Hkv;
   const int b = bh / Ht, h = bh % Ht;
   const InView& v = (h < Hq) ? qv : kv;
@@ -163,6 +165,128 @@ __global__ void __launch_bounds__(D / SA2PP_MEANS_CPT) channel_means_kernel(InVi
     return;
   }
   *reinterpret_cast<double2*>(means + static_cast<int64_t>(bh) * D + 2 * t) = make_double2(s0 / n, s1 / n);
+}
+
+// Parallel exact means for 16-bit inputs.  numpy's sequential FP64 sum rounds nothing when every
+// partial sum is representable: all elements are multiples of u = 2^(E_min - (p - 1)) (E_min the
+// smallest exponent among the channel's nonzero elements, p the input precision) and every partial
+// sum is at most N * max|x|, so N * max|x| < 2^53 * u makes the sequential sum exact and therefore
+// equal to a sum in any order.  means_partial sums kMeansRows-row chunks per channel in FP64
+// and records max|x| and E_min; means_finalize adds the chunks, checks the certificate per channel
+// and writes the mean, or flags the head for the sequential kernel (channel_means_kernel), which
+// then runs only for flagged heads.
+#ifndef SA2PP_MEANS_PAR
+#define SA2PP_MEANS_PAR 1
+#endif
+
+template <typename T>
+__device__ __forceinline__ T __ushort_as_bf16_or_half(unsigned short u);
+template <>
+__device__ __forceinline__ __nv_bfloat16 __ushort_as_bf16_or_half<__nv_bfloat16>(unsigned short u) {
+  return __ushort_as_bfloat16(u);
+}
+template <>
+__device__ __forceinline__ __half __ushort_as_bf16_or_half<__half>(unsigned short u) {
+  return __ushort_as_half(u);
+}
+
+template <typename T>
+struct Bits16;  // exponent/precision of the 16-bit input formats
+template <>
+struct Bits16<__nv_bfloat16> {
+  static constexpr int kMantBits = 7, kBias = 127;
+};
+template <>
+struct Bits16<__half> {
+  static constexpr int kMantBits = 10, kBias = 15;
+};
+
+// 256 threads: lane group of D/8 threads covers a row with 16-byte loads (8 channels each), 256/(D/8)
+// row groups stride the chunk; per-channel FP64 sums and (max |x|, min nonzero |x|) as packed 16-bit
+// SIMD, reduced across row groups in shared memory (exact under the certificate, so order-free)
+template <typename T, int D>
+__global__ void __launch_bounds__(256) means_partial_kernel(InView qv, InView kv, int Hq, int Hkv, int N, int dc,
+                                                            double* __restrict__ part,
+                                                            unsigned long long* __restrict__ stat) {
+  constexpr int LPR = D / 8, RG = 256 / LPR;
+  __shared__ double s_acc[RG][D];
+  __shared__ uint32_t s_mx[RG][D / 2], s_mn[RG][D / 2];
+  const int ch = blockIdx.x, bh = blockIdx.y, n_ch = gridDim.x;
+  const int Ht = Hq + Hkv;
+  const int b = bh / Ht, h = bh % Ht;
+  const InView& v = (h < Hq) ? qv : kv;
+  const int hh = (h < Hq) ? h : h - Hq;
+  const int tid = threadIdx.x, c8 = tid % LPR, rg = tid / LPR, c0 = c8 * 8;
+  const int r0 = ch * kMeansRows, r1 = min(N, r0 + kMeansRows);
+  double acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.0;
+  uint32_t mx[4] = {0u, 0u, 0u, 0u}, mn[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+  if (c0 < dc) {
+#pragma unroll 4
+    for (int r = r0 + rg; r < r1; r += RG) {
+      const uint4 w4 = __ldcs(reinterpret_cast<const uint4*>(row_ptr<T>(v, b, hh, r) + c0));
+      const uint32_t w[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const uint32_t mag = w[i] & 0x7FFF7FFFu;
+        mx[i] = __vmaxu2(mx[i], mag);
+        mn[i] = __vminu2(mn[i], mag | __vcmpeq2(mag, 0u));  // zeros do not count toward the min
+        const float lo = to_f32<T>(__ushort_as_bf16_or_half<T>(static_cast<unsigned short>(w[i] & 0xFFFFu)));
+        const float hi = to_f32<T>(__ushort_as_bf16_or_half<T>(static_cast<unsigned short>(w[i] >> 16)));
+        acc[2 * i] += static_cast<double>(lo);
+        acc[2 * i + 1] += static_cast<double>(hi);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s_acc[rg][c0 + i] = acc[i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    s_mx[rg][c0 / 2 + i] = mx[i];
+    s_mn[rg][c0 / 2 + i] = mn[i];
+  }
+  __syncthreads();
+  if (tid < D) {
+    const int c = tid, sh = (c & 1) * 16;
+    double a = 0.0;
+    uint32_t m = 0u, n = 0xFFFFu;
+    for (int g = 0; g < RG; ++g) {
+      a += s_acc[g][c];
+      m = max(m, (s_mx[g][c / 2] >> sh) & 0xFFFFu);
+      n = min(n, (s_mn[g][c / 2] >> sh) & 0xFFFFu);
+    }
+    const uint32_t emin = n == 0xFFFFu ? 0xFFFFu : max(n >> Bits16<T>::kMantBits, 1u);
+    const int64_t o = (static_cast<int64_t>(bh) * n_ch + ch) * D + c;
+    part[o] = a;
+    stat[o] = (static_cast<unsigned long long>(m) << 32) | emin;
+  }
+}
+
+template <typename T, int D>
+__global__ void __launch_bounds__(D) means_finalize_kernel(const double* __restrict__ part,
+                                                           const unsigned long long* __restrict__ stat, int n_ch,
+                                                           int N, double* __restrict__ means, int* __restrict__ need) {
+  constexpr int MB = Bits16<T>::kMantBits, BIAS = Bits16<T>::kBias;
+  const int bh = blockIdx.x, c = threadIdx.x;
+  double acc = 0.0;
+  uint32_t mx = 0u, emin = 0xFFFFu;
+  for (int k = 0; k < n_ch; ++k) {
+    const int64_t o = (static_cast<int64_t>(bh) * n_ch + k) * D + c;
+    acc += part[o];  // exact when certified, so the order is free
+    const unsigned long long s = stat[o];
+    mx = max(mx, static_cast<uint32_t>(s >> 32));
+    emin = min(emin, static_cast<uint32_t>(s & 0xFFFFu));
+  }
+  bool ok = true;
+  if (mx != 0u) {
+    const float xmax = to_f32<T>(__ushort_as_bf16_or_half<T>(static_cast<unsigned short>(mx)));
+    const int ulp_exp = static_cast<int>(emin) - BIAS - MB;  // u = 2^ulp_exp
+    ok = static_cast<double>(N) * static_cast<double>(xmax) < ldexp(1.0, 53 + ulp_exp);
+  }
+  if (ok) means[static_cast<int64_t>(bh) * D + c] = acc / static_cast<double>(N);
+  const int any_fail = __syncthreads_or(!ok);
+  if (c == 0) need[bh] = any_fail;
 }
 
 // ------------------------------------------------------------------ shared helpers
@@ -947,7 +1071,25 @@ static cudaError_t launch_prepass_t(const PrepassLaunch& L, cudaStream_t st) {
       return cudaFuncSetAttribute(channel_means_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     });
     if (e != cudaSuccess) return e;
-    channel_means_kernel<T, D><<<L.B * Ht, M::kThreads, smem, st>>>(qv, kv, L.Hq, L.Hkv, L.N, L.means, L.d_in);
+    const int* need = nullptr;
+    if constexpr (sizeof(T) == 2) {
+      // fewer (b, head) chains than SMs: the sequential kernel is pure add-chain latency (long
+      // contexts, CogVideoX, the host pipeline's chunks), so the parallel certified path goes first;
+      // with more chains it measured slower (it competes with quantize_v for bandwidth)
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      if (SA2PP_MEANS_PAR && L.ws_means != nullptr && L.B * Ht < sms) {
+        const int n_ch = (L.N + kMeansRows - 1) / kMeansRows;
+        auto* part = static_cast<double*>(L.ws_means);
+        auto* stat = reinterpret_cast<unsigned long long*>(part + static_cast<int64_t>(L.B) * Ht * n_ch * D);
+        int* flags = reinterpret_cast<int*>(stat + static_cast<int64_t>(L.B) * Ht * n_ch * D);
+        means_partial_kernel<T, D><<<dim3(n_ch, L.B * Ht), 256, 0, st>>>(qv, kv, L.Hq, L.Hkv, L.N, L.d_in, part, stat);
+        means_finalize_kernel<T, D><<<L.B * Ht, D, 0, st>>>(part, stat, n_ch, L.N, L.means, flags);
+        need = flags;
+      }
+    }
+    channel_means_kernel<T, D><<<L.B * Ht, M::kThreads, smem, st>>>(qv, kv, L.Hq, L.Hkv, L.N, L.means, L.d_in, need);
   } else {
     cudaMemsetAsync(L.means, 0, sizeof(double) * L.B * Ht * D, st);
   }

@@ -157,7 +157,8 @@ int sa2pp_quant_sizes(const sa2pp_problem* p, sa2pp_quant_sizes_t* s) {
   s->bias = B * Hq * d.np * 4;
   s->bias_l2 = B * Hq * d.np * 4;
   s->means = B * (Hq + Hkv) * D * 8;
-  s->workspace = 0;  // reserved: the current kernels need no scratch
+  // the parallel exact channel means (optional: a smaller or null workspace selects the sequential kernel)
+  s->workspace = sa2pp::means_ws_bytes(B, Hq + Hkv, p->seq_len, D);
   return SA2PP_OK;
 }
 
@@ -196,10 +197,11 @@ int sa2pp_prepass(const sa2pp_problem* p, const sa2pp_inputs* in, const sa2pp_qu
     return rc;
   sa2pp_quant_sizes_t sz;
   sa2pp_quant_sizes(p, &sz);
-  if (ws_bytes < sz.workspace) return fail(SA2PP_ERR_INVALID, "workspace too small: need %zu bytes", sz.workspace);
+
   const Dims d = dims_of(*p);
   sa2pp::PrepassLaunch L{};
   L.dtype = in->dtype;
+  L.ws_means = (ws != nullptr && ws_bytes >= sz.workspace && aligned16(ws)) ? ws : nullptr;
   L.D = sa2pp::padded_dim(p->head_dim);
   L.d_in = p->head_dim;
   L.B = p->batch;

@@ -44,6 +44,14 @@ struct PerDevice {
 // of the real ones unchanged (per-block amax over zeros, per-channel V scales, independent PV columns).
 __host__ __device__ constexpr int padded_dim(int d) { return d <= 64 ? 64 : 128; }
 
+// workspace of the parallel exact channel means: per (b, head, 512-row chunk, channel) an FP64 sum and
+// a 64-bit (max |x|, min exponent) word, plus one flag per (b, head)
+constexpr int kMeansRows = 512;
+inline size_t means_ws_bytes(int64_t B, int64_t Ht, int64_t N, int64_t D) {
+  const int64_t n_ch = (N + kMeansRows - 1) / kMeansRows;
+  return static_cast<size_t>(B * Ht * n_ch * D * 16 + B * Ht * 4);
+}
+
 struct PrepassLaunch {
   int d_in;  // channels present in the inputs (head_dim); D is the padded kernel width
   int dtype, D, B, Hq, Hkv, N, Nq_pad, Np, n_qt, n_kb, qmax, smoothing;
@@ -51,6 +59,7 @@ struct PrepassLaunch {
   const void *q, *k, *v;
   int64_t q_stride[3], k_stride[3], v_stride[3];
   double* means;
+  void* ws_means;  // workspace for the parallel exact means (means_ws_bytes), or null: sequential only
   int8_t* q_codes;
   float* q_scale;
   double* q_scale64;

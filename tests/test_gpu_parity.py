@@ -284,6 +284,34 @@ def test_fp32_inputs_wide_range_means_match_numpy():
     assert np.array_equal(qt.k_scale64[0, 1].cpu().numpy(), ref.k_scale)
 
 
+@pytest.mark.parametrize("dtype,d", [(torch.bfloat16, 128), (torch.float16, 64), (torch.bfloat16, 96)])
+def test_parallel_certified_means_match_numpy(dtype, d):
+    """16-bit inputs with fewer (b, head) chains than SMs take the parallel certified channel-mean
+    path: heads whose certificate holds (N(0,1), all-zero and subnormal-only channels) and heads
+    where it fails (exponents spread over ~2^-60..2^10, so numpy's sequential FP64 sum rounds and the
+    sequential kernel must run) all equal numpy's x.mean(axis=0) bit for bit."""
+    rng = np.random.default_rng(29)
+    N, H = 16384, 3
+    tiny = 1e-40 if dtype == torch.bfloat16 else 6e-8  # subnormal in the input format
+    spread = 12.0 if dtype == torch.bfloat16 else 1.5  # keep fp16 finite
+    x = []
+    for _ in range(2):  # Q, K
+        t = rng.standard_normal((1, H, N, d))
+        t[0, 1] *= np.exp(rng.standard_normal((N, 1)) * spread)
+        t[0, 2, :, 0] = 0.0
+        t[0, 2, :, 1] = tiny * np.sign(rng.standard_normal(N))
+        x.append(torch.from_numpy(t).to(dtype))
+    v = torch.from_numpy(rng.standard_normal((1, H, N, d))).to(dtype)
+    qt = sa.quantize(x[0].cuda(), x[1].cuda(), v.cuda())
+    torch.cuda.synchronize()
+    means = qt.means[0].cpu().numpy()
+    for i, t in enumerate(x):
+        for h in range(H):
+            want = t[0, h].double().numpy().mean(axis=0)
+            assert np.array_equal(means[i * H + h, :d], want), (i, h)
+            assert not means[i * H + h, d:].any()
+
+
 def test_fp32_accumulator_close_to_fp16():
     g = load_golden("attn_bf16_d128")
     c = golden_config(g)
