@@ -645,6 +645,9 @@ __device__ __forceinline__ void load_rows(const InView& in, int b, int h, int n0
 #ifndef SA2PP_K_MINB
 #define SA2PP_K_MINB 3
 #endif
+#ifndef SA2PP_K_RSCATTER
+#define SA2PP_K_RSCATTER 1  // bias: reduce-scatter butterfly instead of a full butterfly per row
+#endif
 // PAD: head_dim < D (32 / 96), threads of the padded channels load nothing (zeros); a separate
 // instantiation so the unpadded kernel keeps its register allocation
 template <typename T, int D, bool PAD>
@@ -830,18 +833,41 @@ __global__ void __launch_bounds__(256, SA2PP_K_MINB) quantize_k_kernel(InView kv
             acc[rr] = fma(q2.y, static_cast<double>(kt[rr].get(i + 1)) - m2.y, acc[rr]);
           }
         }
+#if SA2PP_K_RSCATTER
+        // reduce-scatter over the row's LPR lanes: each halving step keeps half of the live rows
+        // (lanes with bit o set the upper half), so lane c8 ends with row c8 / (LPR / RT) complete
+#pragma unroll
+        for (int w = RT, o = LPR / 2; w > 1; w >>= 1, o >>= 1) {
+          const bool up = (c8 & o) != 0;
+#pragma unroll
+          for (int i = 0; i < w / 2; ++i) {
+            const double send = up ? acc[i] : acc[i + w / 2];
+            const double keep = up ? acc[i + w / 2] : acc[i];
+            acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+#pragma unroll
+        for (int o = LPR / (2 * RT); o > 0; o >>= 1) acc[0] += __shfl_xor_sync(0xffffffffu, acc[0], o);
+#else
 #pragma unroll
         for (int o = 1; o < LPR; o <<= 1) {
 #pragma unroll
           for (int rr = 0; rr < RT; ++rr) acc[rr] += __shfl_xor_sync(0xffffffffu, acc[rr], o);
         }
+#endif
       }
+#if SA2PP_K_RSCATTER
+      if (c8 % (LPR / RT) == 0) {
+        const int r = rg * RT + c8 / (LPR / RT);
+        double a = acc[0];
+#else
       if (c8 < RT) {
         const int r = rg * RT + c8;
         double a = acc[0];
 #pragma unroll
         for (int rr = 1; rr < RT; ++rr)
           if (c8 == rr) a = acc[rr];
+#endif
         if (r >= rows) a = 0.0;
         const int64_t o = (static_cast<int64_t>(b) * Hq + hq) * Np + n0 + r;
         bias[o] = static_cast<float>(a);
