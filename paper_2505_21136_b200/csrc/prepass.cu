@@ -645,6 +645,9 @@ __device__ __forceinline__ void load_rows(const InView& in, int b, int h, int n0
 #ifndef SA2PP_K_MINB
 #define SA2PP_K_MINB 3
 #endif
+#ifndef SA2PP_K_SMEM_SPLIT
+#define SA2PP_K_SMEM_SPLIT 0  // 1: the (hi, lo) split of the K means made once per channel in smem (A/B: profiles/r02/kernel_experiments.md)
+#endif
 #ifndef SA2PP_K_RSCATTER
 #define SA2PP_K_RSCATTER 1  // bias: reduce-scatter butterfly instead of a full butterfly per row
 #endif
@@ -661,6 +664,9 @@ __global__ void __launch_bounds__(256, SA2PP_K_MINB) quantize_k_kernel(InView kv
   constexpr int LPR = G::LPR, RT = G::RT;
   __shared__ float s_kmn[8 * D], s_kmx[8 * D];
   __shared__ double s_red[8];
+#if SA2PP_K_SMEM_SPLIT
+  __shared__ __align__(16) float2 s_mhl[D];  // (hi, lo) float split of the channel means, made once per channel
+#endif
   const int kb = blockIdx.x;
   const int bh = blockIdx.y;
   const int b = bh / Hkv, h = bh % Hkv;
@@ -740,6 +746,12 @@ __global__ void __launch_bounds__(256, SA2PP_K_MINB) quantize_k_kernel(InView kv
       mx = fmaxf(mx, s_kmx[w * D + tid]);
     }
     const double mu = kmu_g[tid];
+#if SA2PP_K_SMEM_SPLIT
+    {
+      const float hi = static_cast<float>(mu);
+      s_mhl[tid] = make_float2(hi, static_cast<float>(mu - static_cast<double>(hi)));
+    }
+#endif
     double amax = 0.0;
     if (mx >= mn) amax = fmax(fabs(static_cast<double>(mx) - mu), fabs(static_cast<double>(mn) - mu));
     double mumax = fabs(mu);
@@ -773,6 +785,14 @@ __global__ void __launch_bounds__(256, SA2PP_K_MINB) quantize_k_kernel(InView kv
   //      byte of the rounded float's bits.  |q| <= qmax + 3e-5 under kfast, so no clamp is needed.
   {
     float2 mh[4], ml[4];
+#if SA2PP_K_SMEM_SPLIT
+#pragma unroll
+    for (int i = 0; i < 8; i += 2) {
+      const float4 a = *reinterpret_cast<const float4*>(&s_mhl[c0 + i]);  // (hi, lo) of c, c + 1
+      mh[i / 2] = make_float2(a.x, a.z);
+      ml[i / 2] = make_float2(a.y, a.w);
+    }
+#else
 #pragma unroll
     for (int i = 0; i < 8; i += 2) {
       const double2 m2 = *reinterpret_cast<const double2*>(kmu_g + c0 + i);
@@ -780,6 +800,7 @@ __global__ void __launch_bounds__(256, SA2PP_K_MINB) quantize_k_kernel(InView kv
       ml[i / 2] = make_float2(static_cast<float>(m2.x - static_cast<double>(mh[i / 2].x)),
                               static_cast<float>(m2.y - static_cast<double>(mh[i / 2].y)));
     }
+#endif
     const float2 inv2 = make_float2(kinv32, kinv32);
     const float2 magic2 = make_float2(12582912.0f, 12582912.0f);
     int8_t* kdst = k_codes + (static_cast<int64_t>(bh) * Np + n0 + rg * RT) * D + c0;
